@@ -1,0 +1,1103 @@
+// pnn_train.cu — fused batched Poisson-NN trainer (forward, Poisson-NLL
+// backward, bias-corrected Adam) for many independent models.
+//
+// Reference semantics (bbcount/pnn.py):
+//   init_model      87-105  U(+-1/sqrt(d)) W1 (row-major), b1; U(+-1/sqrt(h)) W2, b2
+//   forward         108-118 rate = logaddexp(0, tanh(x W1' + b1) . W2 + b2) + eps
+//   loss_and_grads  121-147 loss = mean(rate - y log(rate + eps)); d_rate = (1 - y/(rate+eps))/nb;
+//                           d_z = d_rate exp(z - softplus); d_pre = d_z W2 (1 - a^2)
+//   adam_step       174-189 finite check per block (W1,b1,W2,b2), m/v update, bias correction
+//   train           211-250 per-epoch rng.permutation(n), ceil(n/B) minibatches (short tail kept),
+//                           TrainingError on a non-finite batch loss, history = mean batch loss
+//
+// CTA layout (warp-specialised):
+//   consumer warps : one model per group of G lanes.  Lane g owns hidden units
+//                    j = g, g+G, ... (W1 row, b1, W2 and their Adam moments in
+//                    registers); the only cross-lane traffic per sample is one
+//                    butterfly all-reduce of the output pre-activation.  SC
+//                    minibatch samples are processed together (independent
+//                    dependency chains), and the next chunk's rows are
+//                    prefetched from L2 while the current one computes.
+//   producer warp  : lane i replays model i's NumPy PCG64 stream and writes
+//                    epoch e+1's Fisher-Yates permutation into a shared-memory
+//                    double buffer while the consumer trains on epoch e, so the
+//                    sequential shuffle is off the training critical path.
+//   Hand-off: per-model produced/consumed epoch counters in shared memory.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "launch.h"
+#include "pcg64.cuh"
+
+namespace bbml {
+
+template <typename T>
+struct Arith;
+template <>
+struct Arith<double> {  // numpy elementwise: separately rounded mul/add/div (no FMA)
+  __device__ static __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  __device__ static __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  __device__ static __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+  __device__ static __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+};
+template <>
+struct Arith<float> {  // FP32 kernel: contraction allowed, fast (2 ulp) division
+  __device__ static __forceinline__ float mul(float a, float b) { return a * b; }
+  __device__ static __forceinline__ float add(float a, float b) { return a + b; }
+  __device__ static __forceinline__ float sub(float a, float b) { return a - b; }
+  __device__ static __forceinline__ float div(float a, float b) { return __fdividef(a, b); }
+};
+
+template <typename T>
+__device__ __forceinline__ void adam_update(T& p, T& m, T& v, T g, T bc1, T bc2, T lr) {
+  using A = Arith<T>;
+  const T b1 = T(0.9), b2 = T(0.999);
+  const T c1 = T(1.0 - 0.9), c2 = T(1.0 - 0.999);
+  m = A::add(A::mul(b1, m), A::mul(c1, g));
+  v = A::add(A::mul(b2, v), A::mul(c2, A::mul(g, g)));
+  const T mh = A::div(m, bc1);
+  const T vh = A::div(v, bc2);
+  p = A::sub(p, A::div(A::mul(lr, mh), A::add(f_sqrt(vh), T(1e-8))));
+}
+
+// FP32 Adam with the bias corrections applied as precomputed reciprocals:
+// one sqrt and one division per parameter.
+__device__ __forceinline__ void adam_fast(float& p, float& m, float& v, float g, float i1, float i2,
+                                          float lr) {
+  m = 0.9f * m + 0.1f * g;
+  v = 0.999f * v + 0.001f * (g * g);
+  float s;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(s) : "f"(v * i2));  // MUFU.SQRT
+  p -= __fdividef(lr * (m * i1), s + 1e-8f);
+}
+
+__device__ __forceinline__ float act_tanh(float x) { return tanh_fast(x); }
+__device__ __forceinline__ double act_tanh(double x) { return tanh(x); }
+
+__device__ __forceinline__ int ld_volatile(const int* p) { return *(volatile const int*)p; }
+__device__ __forceinline__ void st_volatile(int* p, int v) { *(volatile int*)p = v; }
+
+constexpr int kConsumedDone = 1 << 30;
+
+// Fisher-Yates of arange(n) from the top index down (Generator.permutation)
+template <typename PermT>
+__device__ __forceinline__ void fisher_yates(Pcg64& rng, PermT* perm, int n) {
+  for (int i = 0; i < n; ++i) perm[i] = (PermT)i;
+  for (int i = n - 1; i > 0; --i) {
+    const int j = (int)rng.interval32((uint32_t)i);
+    const PermT a = perm[i];
+    perm[i] = perm[j];
+    perm[j] = a;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-cooperative permutation producer.
+//
+// numpy's Generator.permutation(n) is Fisher-Yates from i = n-1 down, each j
+// drawn by random_interval(i): masked rejection over the buffered 32-bit
+// PCG64 stream (low half of each next64 first).  The sequential part is only
+// the accept/swap scan; the draws themselves are an LCG, so the warp
+// produces 32 consecutive next64 outputs at once by jump-ahead
+// (s_{k+l} = a^l s_k + inc * sum_{t<l} a^t, per-lane constants), stages the
+// 64 uint32 draws in shared memory, and lane 0 consumes them.  When an epoch
+// ends mid-batch, the stream is rewound to exactly the next64 calls numpy
+// would have made (with the half-consumed high word buffered), so epoch e+1
+// continues bit-identically.
+// ---------------------------------------------------------------------------
+struct ProdModel {
+  unsigned long long s_hi, s_lo, inc_hi, inc_lo;
+  uint32_t buf32;
+  int has32, next_ep, n, epochs, pad0, pad1, pad2;
+};
+
+__device__ __forceinline__ u128 shfl_u128(u128 v, int src) {
+  const unsigned long long hi = __shfl_sync(0xffffffffu, (unsigned long long)(v >> 64), src);
+  const unsigned long long lo = __shfl_sync(0xffffffffu, (unsigned long long)v, src);
+  return ((u128)hi << 64) | lo;
+}
+
+__device__ __forceinline__ unsigned long long xsl_rr(u128 s) {
+  const unsigned long long hi = (unsigned long long)(s >> 64), lo = (unsigned long long)s;
+  const unsigned long long x = hi ^ lo;
+  const unsigned rot = (unsigned)(hi >> 58);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+template <typename PermT>
+__device__ void perm_producer_warp(const PnnLaunch& L, int groups, int pw, int npw, int* produced,
+                                   int* consumed, PermT* sperm, ProdModel* pm, uint32_t* ring) {
+  const int lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
+  // lane l holds A = a^(l+1), Gs = sum_{t<=l} a^t  (s_{k+l+1} = A s_k + Gs * inc)
+  const u128 a = Pcg64::mult();
+  u128 A = a, Gs = 1;
+  for (int t = 0; t < lane; ++t) {
+    A = A * a;
+    Gs = Gs * a + 1;
+  }
+  if (lane == 0) {
+    for (int m = pw; m < groups; m += npw) {
+      const int64_t gid = (int64_t)blockIdx.x * groups + m;
+      ProdModel st{};
+      if (gid < L.n_tasks) {
+        const bbml_pnn_task tk = L.tasks[gid];
+        Pcg64 rng;
+        rng.seed(tk.seed);
+        const int P = tk.h * (tk.d + 2) + 1;
+        for (int i = 0; i < P; ++i) rng.next64();  // init_model draws (pnn.py:100-103)
+        st.s_hi = (unsigned long long)(rng.state >> 64);
+        st.s_lo = (unsigned long long)rng.state;
+        st.inc_hi = (unsigned long long)(rng.inc >> 64);
+        st.inc_lo = (unsigned long long)rng.inc;
+        st.n = tk.n;
+        st.epochs = tk.epochs;
+      }
+      pm[m] = st;
+    }
+  }
+  __syncwarp();
+  while (true) {
+    bool alive = false, progress = false;
+    for (int m = pw; m < groups; m += npw) {
+      const int64_t gid = (int64_t)blockIdx.x * groups + m;
+      if (gid >= L.n_tasks) continue;
+      const int e = pm[m].next_ep;
+      if (e >= pm[m].epochs) continue;
+      const int c = ld_volatile(consumed + m);
+      if (c >= kConsumedDone) {  // consumer stopped (diverged): retire the model
+        __syncwarp();
+        if (lane == 0) pm[m].next_ep = pm[m].epochs;
+        __syncwarp();
+        continue;
+      }
+      alive = true;
+      if (c < e - 1) continue;  // buffer (e & 1) still in use by epoch e - 2
+      const int n = pm[m].n;
+      PermT* perm = (L.perm_in_smem ? sperm + (int64_t)m * 2 * L.perm_cap
+                                    : (PermT*)L.perm_global + 2 * L.perm_offset[gid]) +
+                    (e & 1) * (L.perm_in_smem ? (int64_t)L.perm_cap : (int64_t)n);
+      for (int x = lane; x < n; x += 32) perm[x] = (PermT)x;
+      u128 s = ((u128)pm[m].s_hi << 64) | pm[m].s_lo;
+      const u128 inc = ((u128)pm[m].inc_hi << 64) | pm[m].inc_lo;
+      const u128 C = Gs * inc;
+      int has32 = pm[m].has32;
+      uint32_t buf = pm[m].buf32;
+      int i = n - 1;
+      __syncwarp();
+      if (i > 0 && has32) {
+        if (lane == 0) {
+          const uint32_t v = buf & (0xffffffffu >> __clz(i));
+          if ((int)v <= i) {
+            const PermT t = perm[i];
+            perm[i] = perm[v];
+            perm[v] = t;
+            --i;
+          }
+        }
+        i = __shfl_sync(FULL, i, 0);
+        has32 = 0;
+      }
+      while (i > 0) {
+        const u128 st = A * s + C;
+        const unsigned long long o = xsl_rr(st);
+        ring[2 * lane] = (uint32_t)o;
+        ring[2 * lane + 1] = (uint32_t)(o >> 32);
+        __syncwarp();
+        int q = 0;
+        if (lane == 0) {
+          while (q < 64 && i > 0) {
+            const uint32_t v = ring[q++] & (0xffffffffu >> __clz(i));
+            if ((int)v <= i) {
+              const PermT t = perm[i];
+              perm[i] = perm[v];
+              perm[v] = t;
+              --i;
+            }
+          }
+        }
+        q = __shfl_sync(FULL, q, 0);
+        i = __shfl_sync(FULL, i, 0);
+        if (q < 64) {  // stopped mid-batch: rewind to the next64 calls actually made
+          const int used = (q + 1) >> 1;
+          s = shfl_u128(st, used - 1);
+          has32 = q & 1;
+          buf = has32 ? ring[q] : 0u;
+        } else {
+          s = shfl_u128(st, 31);
+          has32 = 0;
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        pm[m].s_hi = (unsigned long long)(s >> 64);
+        pm[m].s_lo = (unsigned long long)s;
+        pm[m].has32 = has32;
+        pm[m].buf32 = buf;
+        pm[m].next_ep = e + 1;
+        __threadfence_block();
+        st_volatile(produced + m, e + 1);
+      }
+      __syncwarp();
+      progress = true;
+    }
+    if (!alive) break;
+    if (!progress) __nanosleep(100);
+  }
+}
+
+// shared-memory carve-up common to both trainers:
+//   [produced | consumed] ints, ProdModel[groups], ring[npw][64], perm buffers
+struct PnnSmem {
+  int* produced;
+  int* consumed;
+  ProdModel* pm;
+  uint32_t* ring;
+  unsigned char* perm;
+};
+
+__host__ __device__ inline size_t pnn_smem_header(int groups, int npw) {
+  size_t b = 16 * ((2 * groups * sizeof(int) + 15) / 16);
+  b += groups * sizeof(ProdModel);
+  b += npw * 64 * sizeof(uint32_t);
+  return 16 * ((b + 15) / 16);
+}
+
+__device__ inline PnnSmem pnn_smem(unsigned char* raw, int groups, int npw) {
+  PnnSmem S;
+  S.produced = (int*)raw;
+  S.consumed = S.produced + groups;
+  size_t off = 16 * ((2 * groups * sizeof(int) + 15) / 16);
+  S.pm = (ProdModel*)(raw + off);
+  off += groups * sizeof(ProdModel);
+  S.ring = (uint32_t*)(raw + off);
+  S.perm = raw + pnn_smem_header(groups, npw);
+  return S;
+}
+
+template <typename T, int DM, int SC, typename PermT>
+__device__ __forceinline__ void load_chunk(T (&xs)[SC][DM], T (&ys)[SC], const PermT* perm,
+                                           int base, int cnt, const double* __restrict__ X,
+                                           const double* __restrict__ Y, int xs_stride, int d) {
+#pragma unroll
+  for (int c = 0; c < SC; ++c) {
+    const int row = (int)perm[base + (c < cnt ? c : 0)];
+#pragma unroll
+    for (int k = 0; k < DM; ++k)
+      xs[c][k] = (k < d) ? T(__ldg(X + (int64_t)row * xs_stride + k)) : T(0);
+    ys[c] = T(__ldg(Y + row));
+  }
+}
+
+template <typename T, int DM, int HM, int G, int SC, typename PermT>
+__global__ void pnn_train_kernel(PnnLaunch L) {
+  static_assert(G == 1 || G == 2 || G == 4 || G == 8 || G == 16 || G == 32, "group size");
+  constexpr int U = (HM + G - 1) / G;
+  using A = Arith<T>;
+
+  const int groups = L.groups_per_cta;
+  const int cons_threads = ((groups * G + 31) / 32) * 32;
+  const int npw = ((int)blockDim.x - cons_threads) / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const PnnSmem SM = pnn_smem(smem_raw, groups, npw);
+  int* produced = SM.produced;
+  int* consumed = SM.consumed;
+  PermT* sperm = (PermT*)SM.perm;
+  if (threadIdx.x < groups) {
+    produced[threadIdx.x] = 0;
+    consumed[threadIdx.x] = 0;
+  }
+  __syncthreads();
+
+  // ===================== producer warps =====================
+  if ((int)threadIdx.x >= cons_threads) {
+    const int pw = ((int)threadIdx.x - cons_threads) >> 5;
+    perm_producer_warp<PermT>(L, groups, pw, npw, produced, consumed, sperm, SM.pm, SM.ring + 64 * pw);
+    return;
+  }
+
+  // ===================== consumer groups =====================
+  const int lane = threadIdx.x & 31;
+  const int g = threadIdx.x % G;
+  const int gi = threadIdx.x / G;
+  const int64_t gid = (int64_t)blockIdx.x * groups + gi;
+  if (gi >= groups || gid >= L.n_tasks) return;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+
+  const bbml_pnn_task tk = L.tasks[gid];
+  const int orig = L.orig_index[gid];
+  const int n = tk.n, d = tk.d, h = tk.h, B = tk.batch;
+  const double* __restrict__ X = L.X + tk.row_begin * (int64_t)L.x_stride;
+  const double* __restrict__ Y = L.y + tk.row_begin;
+  const PermT* pbase = L.perm_in_smem ? sperm + (int64_t)gi * 2 * L.perm_cap
+                                      : (const PermT*)L.perm_global + 2 * L.perm_offset[gid];
+  const int64_t cap = L.perm_in_smem ? L.perm_cap : n;
+
+  // ---- init (pnn.py:97-104): every lane replays the P draws, keeps its own
+  T w1[U][DM], b1[U], w2[U];
+  T mw1[U][DM], vw1[U][DM], mb1[U], vb1[U], mw2[U], vw2[U];
+  T b2;
+  {
+    Pcg64 rng;
+    rng.seed(tk.seed);
+    const double s1 = __ddiv_rn(1.0, __dsqrt_rn((double)d));
+    const double s2 = __ddiv_rn(1.0, __dsqrt_rn((double)h));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      b1[u] = w2[u] = mb1[u] = vb1[u] = mw2[u] = vw2[u] = T(0);
+#pragma unroll
+      for (int k = 0; k < DM; ++k) w1[u][k] = mw1[u][k] = vw1[u][k] = T(0);
+    }
+    for (int j = 0; j < h; ++j)
+      for (int k = 0; k < d; ++k) {
+        const double v = rng.uniform(-s1, s1);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int kk = 0; kk < DM; ++kk)
+            if (j == g + u * G && kk == k) w1[u][kk] = T(v);
+      }
+    for (int j = 0; j < h; ++j) {
+      const double v = rng.uniform(-s1, s1);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (j == g + u * G) b1[u] = T(v);
+    }
+    for (int j = 0; j < h; ++j) {
+      const double v = rng.uniform(-s2, s2);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (j == g + u * G) w2[u] = T(v);
+    }
+    b2 = T(rng.uniform(-s2, s2));
+  }
+  T mb2 = T(0), vb2 = T(0);
+  const T eps = T(tk.eps), lr = T(tk.lr);
+
+  int64_t t = 0;
+  double p1 = 1.0, p2 = 1.0;  // running beta^t (FP32 path only)
+  int status = BBML_MODEL_OK, fail_epoch = 0, fail_block = 0;
+  double fail_value = 0.0;
+  const int nbatches = (n + B - 1) / B;
+
+  T gw1[U][DM], gb1[U], gw2[U], gb2;
+  auto zero_grads = [&]() {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      gb1[u] = gw2[u] = T(0);
+#pragma unroll
+      for (int k = 0; k < DM; ++k) gw1[u][k] = T(0);
+    }
+    gb2 = T(0);
+  };
+
+  for (int ep = 0; ep < tk.epochs; ++ep) {
+    while (ld_volatile(produced + gi) <= ep) {
+    }
+    __threadfence_block();
+    const PermT* perm = pbase + (ep & 1) * cap;
+    double epoch_loss = 0.0;
+    zero_grads();
+    T bloss = T(0);
+
+    int bs = 0, s0 = 0;
+    T xs[SC][DM], ys[SC];
+    load_chunk<T, DM, SC, PermT>(xs, ys, perm, 0, min(SC, min(B, n)), X, Y, L.x_stride, d);
+    while (true) {
+      const int nb = min(B, n - bs);
+      const int cnt = min(SC, nb - s0);
+      int nbs = bs, ns0 = s0 + SC;
+      if (ns0 >= nb) {
+        nbs = bs + B;
+        ns0 = 0;
+      }
+      const bool more = nbs < n;
+      T nx[SC][DM], ny[SC];
+      if (more) {
+        const int nnb = min(B, n - nbs);
+        load_chunk<T, DM, SC, PermT>(nx, ny, perm, nbs + ns0, min(SC, nnb - ns0), X, Y,
+                                     L.x_stride, d);
+      }
+      // ---- forward: owned hidden units, partial output pre-activation
+      T a[SC][U], zs[SC];
+#pragma unroll
+      for (int c = 0; c < SC; ++c) {
+        T zp = T(0);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          T pre = b1[u];
+#pragma unroll
+          for (int k = 0; k < DM; ++k) pre += w1[u][k] * xs[c][k];
+          a[c][u] = f_tanh(pre);
+          zp += a[c][u] * w2[u];
+        }
+        zs[c] = zp;
+      }
+#pragma unroll
+      for (int m = 1; m < G; m <<= 1)
+#pragma unroll
+        for (int c = 0; c < SC; ++c) zs[c] += shfl_xor(zs[c], m, gmask, G);
+      // ---- loss and back-propagation through softplus
+      const T nb_t = T(nb);
+#pragma unroll
+      for (int c = 0; c < SC; ++c) {
+        const bool valid = c < cnt;
+        const T z = zs[c] + b2;
+        const T sp = softplus(z);
+        const T rate = A::add(sp, eps);
+        const T re = A::add(rate, eps);
+        const T lc = A::sub(rate, A::mul(ys[c], f_log(re)));
+        const T drate = A::div(A::sub(T(1), A::div(ys[c], re)), nb_t);
+        const T dz = valid ? A::mul(drate, f_exp(A::sub(z, sp))) : T(0);
+        if (valid) bloss += lc;
+        gb2 += dz;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const T av = a[c][u];
+          gw2[u] += av * dz;
+          const T dp = A::mul(A::mul(dz, w2[u]), A::sub(T(1), A::mul(av, av)));
+          gb1[u] += dp;
+#pragma unroll
+          for (int k = 0; k < DM; ++k) gw1[u][k] += dp * xs[c][k];
+        }
+      }
+      if (ns0 == 0) {  // ---- end of minibatch: checks + Adam (pnn.py:243-247)
+        const T loss = A::div(bloss, nb_t);
+        if (!f_finite(loss)) {
+          status = BBML_MODEL_DIVERGED;
+          fail_epoch = ep;
+          fail_value = (double)loss;
+          break;
+        }
+        bool bad_w1 = false, bad_b1 = false, bad_w2 = false;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int k = 0; k < DM; ++k) bad_w1 |= !f_finite(gw1[u][k]);
+          bad_b1 |= !f_finite(gb1[u]);
+          bad_w2 |= !f_finite(gw2[u]);
+        }
+        bad_w1 = __any_sync(gmask, bad_w1);
+        bad_b1 = __any_sync(gmask, bad_b1);
+        bad_w2 = __any_sync(gmask, bad_w2);
+        if (bad_w1 || bad_b1 || bad_w2 || !f_finite(gb2)) {
+          status = BBML_MODEL_NONFINITE_GRAD;
+          fail_epoch = ep;
+          fail_block = bad_w1 ? 0 : bad_b1 ? 1 : bad_w2 ? 2 : 3;
+          break;
+        }
+        ++t;
+        T bc1, bc2;
+        if (sizeof(T) == 8) {
+          bc1 = T(1.0 - pow(0.9, (double)t));
+          bc2 = T(1.0 - pow(0.999, (double)t));
+        } else {
+          p1 *= 0.9;
+          p2 *= 0.999;
+          bc1 = T(1.0 - p1);
+          bc2 = T(1.0 - p2);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int k = 0; k < DM; ++k)
+            adam_update(w1[u][k], mw1[u][k], vw1[u][k], gw1[u][k], bc1, bc2, lr);
+          adam_update(b1[u], mb1[u], vb1[u], gb1[u], bc1, bc2, lr);
+          adam_update(w2[u], mw2[u], vw2[u], gw2[u], bc1, bc2, lr);
+        }
+        adam_update(b2, mb2, vb2, gb2, bc1, bc2, lr);
+        epoch_loss += (double)loss;
+        zero_grads();
+        bloss = T(0);
+      }
+      if (!more) break;
+#pragma unroll
+      for (int c = 0; c < SC; ++c) {
+        ys[c] = ny[c];
+#pragma unroll
+        for (int k = 0; k < DM; ++k) xs[c][k] = nx[c][k];
+      }
+      bs = nbs;
+      s0 = ns0;
+    }
+    __syncwarp(gmask);  // every lane is done reading this epoch's buffer
+    if (status != BBML_MODEL_OK) break;
+    if (g == 0) {
+      if (tk.hist_offset >= 0) L.history[tk.hist_offset + ep] = epoch_loss / nbatches;
+      __threadfence_block();
+      st_volatile(consumed + gi, ep + 1);
+    }
+  }
+  if (g == 0) st_volatile(consumed + gi, kConsumedDone);  // release the producer lane
+
+  // ---- outputs (pack order)
+  double* W = L.weights + tk.w_offset;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int j = g + u * G;
+    if (j < h) {
+#pragma unroll
+      for (int kk = 0; kk < DM; ++kk)
+        if (kk < d) W[j * d + kk] = (double)w1[u][kk];
+      W[h * d + j] = (double)b1[u];
+      W[h * d + h + j] = (double)w2[u];
+    }
+  }
+  if (g == 0) {
+    W[h * d + 2 * h] = (double)b2;
+    bbml_model_status st{};
+    st.code = status;
+    st.epochs = status == BBML_MODEL_OK ? tk.epochs : fail_epoch;
+    st.detail = fail_block;
+    st.value = fail_value;
+    L.status[orig] = st;
+  }
+}
+
+// ------------------------------------------------------------------------
+// Latency-optimised kernel for h <= 16 (the reference default is h = 10):
+// one model per warp.  lane = (sample half sg, hidden unit j): the 16-lane
+// half sg owns samples [sg*SP, sg*SP+SP) of each chunk of 2*SP minibatch
+// samples, lane j owns unit j (its parameters and Adam moments are
+// replicated in both halves and stay bitwise identical).  Per chunk:
+//   forward    : SP tanh per lane, z all-reduced over the 16 units (4 shfl)
+//   loss chain : lane j < SP runs sample j's softplus / log / exp / div chain
+//                once (instead of every lane repeating every sample), then
+//                d_z is broadcast with SP shuffles
+//   backward   : per-unit gradient sums over the lane's SP samples, then one
+//                xor-16 shuffle joins the halves at the end of the minibatch
+// ------------------------------------------------------------------------
+template <typename T, int DM, int SP, typename PermT>
+__global__ void pnn_lat_kernel(PnnLaunch L) {
+  using A = Arith<T>;
+  const int groups = L.groups_per_cta;  // one model per consumer warp
+  const int cons_threads = groups * 32;
+  const int npw = ((int)blockDim.x - cons_threads) / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const PnnSmem SM = pnn_smem(smem_raw, groups, npw);
+  int* produced = SM.produced;
+  int* consumed = SM.consumed;
+  PermT* sperm = (PermT*)SM.perm;
+  if (threadIdx.x < groups) {
+    produced[threadIdx.x] = 0;
+    consumed[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x >= cons_threads) {
+    const int pw = ((int)threadIdx.x - cons_threads) >> 5;
+    perm_producer_warp<PermT>(L, groups, pw, npw, produced, consumed, sperm, SM.pm, SM.ring + 64 * pw);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int gi = threadIdx.x >> 5;
+  const int64_t gid = (int64_t)blockIdx.x * groups + gi;
+  if (gid >= L.n_tasks) return;
+  const int sg = lane >> 4, j = lane & 15;
+  const unsigned FULL = 0xffffffffu;
+
+  const bbml_pnn_task tk = L.tasks[gid];
+  const int orig = L.orig_index[gid];
+  const int n = tk.n, d = tk.d, h = tk.h, B = tk.batch;
+  const double* __restrict__ X = L.X + tk.row_begin * (int64_t)L.x_stride;
+  const double* __restrict__ Y = L.y + tk.row_begin;
+  const PermT* pbase = L.perm_in_smem ? sperm + (int64_t)gi * 2 * L.perm_cap
+                                      : (const PermT*)L.perm_global + 2 * L.perm_offset[gid];
+  const int64_t cap = L.perm_in_smem ? L.perm_cap : n;
+
+  // ---- init (pnn.py:97-104)
+  T w1[DM], b1 = T(0), w2 = T(0), b2;
+  T mw1[DM], vw1[DM], mb1 = T(0), vb1 = T(0), mw2 = T(0), vw2 = T(0), mb2 = T(0), vb2 = T(0);
+#pragma unroll
+  for (int k = 0; k < DM; ++k) w1[k] = mw1[k] = vw1[k] = T(0);
+  {
+    Pcg64 rng;
+    rng.seed(tk.seed);
+    const double s1 = __ddiv_rn(1.0, __dsqrt_rn((double)d));
+    const double s2 = __ddiv_rn(1.0, __dsqrt_rn((double)h));
+    for (int jj = 0; jj < h; ++jj)
+      for (int k = 0; k < d; ++k) {
+        const double v = rng.uniform(-s1, s1);
+#pragma unroll
+        for (int kk = 0; kk < DM; ++kk)
+          if (jj == j && kk == k) w1[kk] = T(v);
+      }
+    for (int jj = 0; jj < h; ++jj) {
+      const double v = rng.uniform(-s1, s1);
+      if (jj == j) b1 = T(v);
+    }
+    for (int jj = 0; jj < h; ++jj) {
+      const double v = rng.uniform(-s2, s2);
+      if (jj == j) w2 = T(v);
+    }
+    b2 = T(rng.uniform(-s2, s2));
+  }
+  const T eps = T(tk.eps), lr = T(tk.lr);
+
+  int64_t t = 0;
+  double p1 = 1.0, p2 = 1.0;
+  int status = BBML_MODEL_OK, fail_epoch = 0, fail_block = 0;
+  double fail_value = 0.0;
+  const int nbatches = (n + B - 1) / B;
+  constexpr int C = 2 * SP;
+
+  T gw1[DM], gb1, gw2, gb2, bloss;
+  auto zero_grads = [&]() {
+#pragma unroll
+    for (int k = 0; k < DM; ++k) gw1[k] = T(0);
+    gb1 = gw2 = gb2 = bloss = T(0);
+  };
+  // rows of samples [off + sg*SP, off + sg*SP + SP) of the chunk (clamped to
+  // valid); the FP32 kernel reads the pre-converted float rows so the
+  // prefetched values land directly in their registers (no conversion stall)
+  const int rstride = sizeof(T) == 8 ? L.x_stride : L.xf_stride;
+  const T* __restrict__ XT = (sizeof(T) == 8 ? (const T*)(const void*)L.X : (const T*)(const void*)L.Xf) +
+                             tk.row_begin * (int64_t)rstride;
+  const T* __restrict__ YT = (sizeof(T) == 8 ? (const T*)(const void*)L.y : (const T*)(const void*)L.yf) +
+                             tk.row_begin;
+  const bool vec4 = sizeof(T) == 4 && DM <= 4 && rstride == 4;
+  const bool y_in_x = vec4 && L.y_in_x;
+  auto load = [&](T (&xs)[SP][DM], T (&ys)[SP], const PermT* perm, int off, int cnt) {
+#pragma unroll
+    for (int i = 0; i < SP; ++i) {
+      const int c = sg * SP + i;
+      const int row = (int)perm[off + (c < cnt ? c : 0)];
+      if constexpr (sizeof(T) == 4 && DM <= 4) {
+        if (vec4) {
+          const float4 v = __ldg((const float4*)(XT + (int64_t)row * 4));
+          const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int k = 0; k < DM; ++k) xs[i][k] = (k < d) ? e[k] : 0.0f;
+          ys[i] = y_in_x ? v.w : __ldg(YT + row);
+          continue;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < DM; ++k) xs[i][k] = (k < d) ? __ldg(XT + (int64_t)row * rstride + k) : T(0);
+      ys[i] = __ldg(YT + row);
+    }
+  };
+
+  for (int ep = 0; ep < tk.epochs; ++ep) {
+    while (ld_volatile(produced + gi) <= ep) {
+    }
+    __threadfence_block();
+    const PermT* perm = pbase + (ep & 1) * cap;
+    T eloss = T(0);
+    zero_grads();
+    int bs = 0, s0 = 0;
+    T xs[SP][DM], ys[SP];
+    load(xs, ys, perm, 0, min(C, min(B, n)));
+    while (true) {
+      const int nb = min(B, n - bs);
+      const int cnt = min(C, nb - s0);
+      int nbs = bs, ns0 = s0 + C;
+      if (ns0 >= nb) {
+        nbs = bs + B;
+        ns0 = 0;
+      }
+      const bool more = nbs < n;
+      T nx[SP][DM], ny[SP];
+      if (more) load(nx, ny, perm, nbs + ns0, min(C, min(B, n - nbs) - ns0));
+
+      // forward
+      T a[SP], z[SP];
+#pragma unroll
+      for (int i = 0; i < SP; ++i) {
+        T pre = b1;
+#pragma unroll
+        for (int k = 0; k < DM; ++k) pre += w1[k] * xs[i][k];
+        a[i] = act_tanh(pre);
+        z[i] = a[i] * w2;
+      }
+#pragma unroll
+      for (int m = 1; m < 16; m <<= 1)
+#pragma unroll
+        for (int i = 0; i < SP; ++i) z[i] += __shfl_xor_sync(FULL, z[i], m);
+      // loss chain of sample (sg, j) on lane j < SP
+      T zj = z[0], yj = ys[0];
+#pragma unroll
+      for (int i = 1; i < SP; ++i)
+        if (j == i) {
+          zj = z[i];
+          yj = ys[i];
+        }
+      const bool mine = j < SP && (sg * SP + j) < cnt;
+      const T nb_t = T(nb);
+      const T zz = zj + b2;
+      const T sp = softplus(zz);
+      const T rate = A::add(sp, eps);
+      const T re = A::add(rate, eps);
+      const T drate = A::div(A::sub(T(1), A::div(yj, re)), nb_t);
+      const T dzj = mine ? A::mul(drate, f_exp(A::sub(zz, sp))) : T(0);
+      if (mine) bloss += A::sub(rate, A::mul(yj, f_log(re)));
+      // backward (own unit, own half's samples)
+#pragma unroll
+      for (int i = 0; i < SP; ++i) {
+        const T dz = __shfl_sync(FULL, dzj, (lane & 16) | i);
+        gb2 += dz;
+        gw2 += a[i] * dz;
+        const T dp = A::mul(A::mul(dz, w2), A::sub(T(1), A::mul(a[i], a[i])));
+        gb1 += dp;
+#pragma unroll
+        for (int k = 0; k < DM; ++k) gw1[k] += dp * xs[i][k];
+      }
+      if (ns0 == 0) {  // end of minibatch
+#pragma unroll
+        for (int k = 0; k < DM; ++k) gw1[k] += __shfl_xor_sync(FULL, gw1[k], 16);
+        gb1 += __shfl_xor_sync(FULL, gb1, 16);
+        gw2 += __shfl_xor_sync(FULL, gw2, 16);
+        gb2 += __shfl_xor_sync(FULL, gb2, 16);
+        // one warp-wide OR of every finiteness predicate (loss first, then the
+        // adam_step block order W1, b1, W2, b2; pnn.py:244-245, 180-183)
+        bool bw1 = false;
+#pragma unroll
+        for (int k = 0; k < DM; ++k) bw1 |= !f_finite(gw1[k]);
+        const unsigned bits = (!f_finite(bloss) ? 1u : 0u) | (bw1 ? 2u : 0u) |
+                              (!f_finite(gb1) ? 4u : 0u) | (!f_finite(gw2) ? 8u : 0u) |
+                              (!f_finite(gb2) ? 16u : 0u);
+        const unsigned any = __reduce_or_sync(FULL, bits);
+        if (any) {
+          T lsum = bloss;
+#pragma unroll
+          for (int m = 1; m < 32; m <<= 1) lsum += __shfl_xor_sync(FULL, lsum, m);
+          const T loss = A::div(lsum, nb_t);
+          if ((any & 1u) || !f_finite(loss)) {
+            status = BBML_MODEL_DIVERGED;
+            fail_epoch = ep;
+            fail_value = (double)loss;
+            break;
+          }
+          status = BBML_MODEL_NONFINITE_GRAD;
+          fail_epoch = ep;
+          fail_block = (any & 2u) ? 0 : (any & 4u) ? 1 : (any & 8u) ? 2 : 3;
+          break;
+        }
+        ++t;
+        if constexpr (sizeof(T) == 8) {
+          const T bc1 = T(1.0 - pow(0.9, (double)t));
+          const T bc2 = T(1.0 - pow(0.999, (double)t));
+#pragma unroll
+          for (int k = 0; k < DM; ++k) adam_update(w1[k], mw1[k], vw1[k], gw1[k], bc1, bc2, lr);
+          adam_update(b1, mb1, vb1, gb1, bc1, bc2, lr);
+          adam_update(w2, mw2, vw2, gw2, bc1, bc2, lr);
+          adam_update(b2, mb2, vb2, gb2, bc1, bc2, lr);
+        } else {
+          p1 *= 0.9;
+          p2 *= 0.999;
+          const T i1 = __fdividef(1.0f, (float)(1.0 - p1)), i2 = __fdividef(1.0f, (float)(1.0 - p2));
+#pragma unroll
+          for (int k = 0; k < DM; ++k) adam_fast(w1[k], mw1[k], vw1[k], gw1[k], i1, i2, lr);
+          adam_fast(b1, mb1, vb1, gb1, i1, i2, lr);
+          adam_fast(w2, mw2, vw2, gw2, i1, i2, lr);
+          adam_fast(b2, mb2, vb2, gb2, i1, i2, lr);
+        }
+        eloss += A::div(bloss, nb_t);  // this lane's share of the batch mean
+        zero_grads();
+      }
+      if (!more) break;
+#pragma unroll
+      for (int i = 0; i < SP; ++i) {
+        ys[i] = ny[i];
+#pragma unroll
+        for (int k = 0; k < DM; ++k) xs[i][k] = nx[i][k];
+      }
+      bs = nbs;
+      s0 = ns0;
+    }
+    __syncwarp();
+    if (status != BBML_MODEL_OK) break;
+    if (tk.hist_offset >= 0) {
+      double el = (double)eloss;
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1) el += __shfl_xor_sync(FULL, el, m);
+      if (lane == 0) L.history[tk.hist_offset + ep] = el / nbatches;
+    }
+    if (lane == 0) {
+      __threadfence_block();
+      st_volatile(consumed + gi, ep + 1);
+    }
+  }
+  if (lane == 0) st_volatile(consumed + gi, kConsumedDone);
+
+  double* W = L.weights + tk.w_offset;
+  if (sg == 0 && j < h) {
+#pragma unroll
+    for (int kk = 0; kk < DM; ++kk)
+      if (kk < d) W[j * d + kk] = (double)w1[kk];
+    W[h * d + j] = (double)b1;
+    W[h * d + h + j] = (double)w2;
+  }
+  if (lane == 0) {
+    W[h * d + 2 * h] = (double)b2;
+    bbml_model_status st{};
+    st.code = status;
+    st.epochs = status == BBML_MODEL_OK ? tk.epochs : fail_epoch;
+    st.detail = fail_block;
+    st.value = fail_value;
+    L.status[orig] = st;
+  }
+}
+
+// ------------------------------------------------------------------------
+// host dispatch
+// ------------------------------------------------------------------------
+
+// FP32 row copy: 16-byte rows {x0..x3} when x_stride <= 4, with y folded
+// into slot 3 when x_stride <= 3 (one LDG.128 per sample in the hot loop).
+__global__ void to_float_kernel(const double* __restrict__ X, int xs, float* __restrict__ Xf,
+                                int xfs, const double* __restrict__ y, float* __restrict__ yf,
+                                int64_t rows) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    for (int k = 0; k < xfs; ++k) Xf[r * xfs + k] = k < xs ? (float)X[r * xs + k] : 0.0f;
+    const float yv = (float)y[r];
+    yf[r] = yv;
+    if (xs <= 3 && xfs == 4) Xf[r * 4 + 3] = yv;
+  }
+}
+
+static int bucket_d(int d) { return d <= 2 ? 2 : d <= 4 ? 4 : 16; }
+static int bucket_h(int h) { return h <= 16 ? 16 : 64; }
+
+template <typename T, int DM, int HM, typename PermT>
+static cudaError_t launch_variant(PnnLaunch L, int64_t nmax, size_t smem_limit, cudaStream_t s) {
+  constexpr bool LAT = HM <= 16;  // h <= 16: warp-per-model latency kernel
+  constexpr int G = 32;
+  constexpr int SC = 10;
+  // models per CTA; each model gets its own warp-cooperative producer warp
+  // (one sequential Fisher-Yates scan keeps up with one consumer warp)
+  const int groups_max = 4;
+  const size_t flags = pnn_smem_header(groups_max, groups_max);
+  const size_t per_group = 2 * (size_t)nmax * sizeof(PermT);
+  int groups = (int)std::min<size_t>(groups_max, (smem_limit - flags) / per_group);
+  size_t smem;
+  if (groups >= 1) {
+    L.perm_in_smem = 1;
+    L.perm_cap = (int32_t)nmax;
+    smem = pnn_smem_header(groups, groups) + (size_t)groups * per_group;
+  } else {
+    groups = groups_max;
+    L.perm_in_smem = 0;
+    L.perm_cap = 0;
+    smem = pnn_smem_header(groups, groups);
+  }
+  L.groups_per_cta = groups;
+  const int cons = ((groups * G + 31) / 32) * 32;
+  const int prod = 32 * groups;
+  const int blocks = (int)ceil_div(L.n_tasks, groups);
+  auto k = LAT ? pnn_lat_kernel<T, DM, 5, PermT> : pnn_train_kernel<T, DM, HM, G, SC, PermT>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k<<<blocks, cons + prod, smem, s>>>(L);
+  return cudaGetLastError();
+}
+
+template <typename T, int DM, int HM>
+static cudaError_t launch_dm_hm(const PnnLaunch& L, int64_t nmax, size_t smem_limit,
+                                cudaStream_t s) {
+  if (nmax <= 65535) return launch_variant<T, DM, HM, uint16_t>(L, nmax, smem_limit, s);
+  return launch_variant<T, DM, HM, int32_t>(L, nmax, smem_limit, s);
+}
+
+template <typename T>
+static cudaError_t launch_bucket(int dm, int hm, const PnnLaunch& L, int64_t nmax,
+                                 size_t smem_limit, cudaStream_t s) {
+  if (dm <= 2) {
+    return hm <= 16 ? launch_dm_hm<T, 2, 16>(L, nmax, smem_limit, s)
+                    : launch_dm_hm<T, 2, 64>(L, nmax, smem_limit, s);
+  } else if (dm <= 4) {
+    return hm <= 16 ? launch_dm_hm<T, 4, 16>(L, nmax, smem_limit, s)
+                    : launch_dm_hm<T, 4, 64>(L, nmax, smem_limit, s);
+  }
+  return hm <= 16 ? launch_dm_hm<T, 16, 16>(L, nmax, smem_limit, s)
+                  : launch_dm_hm<T, 16, 64>(L, nmax, smem_limit, s);
+}
+
+bbml_status pnn_train_launch(const bbml_pnn_task* tasks, int32_t n_tasks, const double* X,
+                             const double* y, int32_t x_stride, double* weights, double* history,
+                             bbml_model_status* status, int32_t precision, cudaStream_t stream) {
+  std::vector<int> idx(n_tasks);
+  for (int i = 0; i < n_tasks; ++i) {
+    const bbml_pnn_task& t = tasks[i];
+    if (t.n < 1 || t.d < 1 || t.h < 1 || t.epochs < 1 || t.batch < 1 || t.row_begin < 0 ||
+        t.w_offset < 0 || t.seed.n_words < 1 || t.seed.n_words > BBML_MAX_ENTROPY_WORDS) {
+      set_error("pnn task %d: invalid field", i);
+      return BBML_ERR_INVALID;
+    }
+    if (t.d > BBML_MAX_INPUTS || t.h > BBML_PNN_MAX_HIDDEN) {
+      set_error("pnn task %d: d=%d h=%d outside the supported envelope", i, t.d, t.h);
+      return BBML_ERR_UNSUPPORTED;
+    }
+    if (t.hist_offset >= 0 && history == nullptr) {
+      set_error("pnn task %d: history requested but history == NULL", i);
+      return BBML_ERR_INVALID;
+    }
+    idx[i] = i;
+  }
+  auto cost = [&](int i) {
+    const bbml_pnn_task& t = tasks[i];
+    return (double)t.epochs * (double)((t.n + t.batch - 1) / t.batch);
+  };
+  // homogeneous launches per (d, h) bucket; longest sequential chains first
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+    const int ka = bucket_d(tasks[a].d) * 1000 + bucket_h(tasks[a].h);
+    const int kb = bucket_d(tasks[b].d) * 1000 + bucket_h(tasks[b].h);
+    if (ka != kb) return ka < kb;
+    return cost(a) > cost(b);
+  });
+  std::vector<bbml_pnn_task> sorted(n_tasks);
+  std::vector<int32_t> orig(n_tasks);
+  std::vector<int64_t> poff(n_tasks);
+  int64_t total = 0;
+  for (int i = 0; i < n_tasks; ++i) {
+    sorted[i] = tasks[idx[i]];
+    orig[i] = idx[i];
+    poff[i] = total;
+    total += sorted[i].n;
+  }
+  ScratchBuffer scratch(stream);
+  bbml_pnn_task* d_tasks = nullptr;
+  int32_t* d_orig = nullptr;
+  int64_t* d_poff = nullptr;
+  bbml_status st;
+  if ((st = scratch.alloc(&d_tasks, n_tasks)) != BBML_OK) return st;
+  if ((st = scratch.alloc(&d_orig, n_tasks)) != BBML_OK) return st;
+  if ((st = scratch.alloc(&d_poff, n_tasks)) != BBML_OK) return st;
+  if ((st = scratch.upload(d_tasks, sorted.data(), n_tasks)) != BBML_OK) return st;
+  if ((st = scratch.upload(d_orig, orig.data(), n_tasks)) != BBML_OK) return st;
+  if ((st = scratch.upload(d_poff, poff.data(), n_tasks)) != BBML_OK) return st;
+
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int smem_optin = 0;
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t smem_limit = std::min<size_t>((size_t)smem_optin, 200 * 1024);
+
+  float* d_xf = nullptr;  // FP32 kernels: one conversion pass over the rows they read
+  float* d_yf = nullptr;
+  int xf_stride = x_stride;
+  if (precision == 32) {
+    int64_t rows = 0;
+    for (int i = 0; i < n_tasks; ++i) rows = std::max<int64_t>(rows, sorted[i].row_begin + sorted[i].n);
+    xf_stride = x_stride <= 4 ? 4 : x_stride;
+    if ((st = scratch.alloc(&d_xf, rows * xf_stride)) != BBML_OK) return st;
+    if ((st = scratch.alloc(&d_yf, rows)) != BBML_OK) return st;
+    to_float_kernel<<<(int)std::min<int64_t>(ceil_div(rows, 256), 4096), 256, 0, stream>>>(
+        X, x_stride, d_xf, xf_stride, y, d_yf, rows);
+  }
+  int32_t* d_perm = nullptr;  // global double-buffer workspace, only if some bucket needs it
+  int begin = 0;
+  while (begin < n_tasks) {
+    const int dm = bucket_d(sorted[begin].d), hm = bucket_h(sorted[begin].h);
+    int end = begin;
+    int64_t nmax = 0;
+    while (end < n_tasks && bucket_d(sorted[end].d) == dm && bucket_h(sorted[end].h) == hm) {
+      nmax = std::max<int64_t>(nmax, sorted[end].n);
+      ++end;
+    }
+    const size_t elem = nmax <= 65535 ? 2 : 4;
+    if (2 * (size_t)nmax * elem + 64 > smem_limit && d_perm == nullptr) {
+      if ((st = scratch.alloc(&d_perm, 2 * total)) != BBML_OK) return st;
+    }
+    PnnLaunch L{};
+    L.tasks = d_tasks + begin;
+    L.orig_index = d_orig + begin;
+    L.perm_offset = d_poff + begin;
+    L.n_tasks = end - begin;
+    L.X = X;
+    L.y = y;
+    L.Xf = d_xf;
+    L.yf = d_yf;
+    L.xf_stride = xf_stride;
+    L.y_in_x = (precision == 32 && x_stride <= 3) ? 1 : 0;
+    L.x_stride = x_stride;
+    L.weights = weights;
+    L.history = history;
+    L.status = status;
+    L.perm_global = d_perm;
+    cudaError_t e = precision == 32 ? launch_bucket<float>(dm, hm, L, nmax, smem_limit, stream)
+                                    : launch_bucket<double>(dm, hm, L, nmax, smem_limit, stream);
+    if (e != cudaSuccess) return cuda_status(e, "pnn_train launch");
+    begin = end;
+  }
+  return scratch.release();
+}
+
+}  // namespace bbml
+
+// ------------------------------------------------------------------------
+// unit level: pnn.loss_and_grads (pnn.py:121-147) for one (model, batch) per
+// thread, FP64.  Used by the drop-in loss_and_grads and the FD-gradient tests.
+// ------------------------------------------------------------------------
+namespace bbml {
+
+__global__ void pnn_loss_grad_kernel(const bbml_pred_task* __restrict__ tasks, int n_tasks,
+                                     const double* __restrict__ X, const double* __restrict__ Y,
+                                     int xs, const double* __restrict__ weights, double nll_eps,
+                                     double* __restrict__ loss, double* __restrict__ grads) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_tasks) return;
+  const bbml_pred_task tk = tasks[i];
+  const int d = tk.d, h = tk.h, n = tk.n;
+  const int hd = h * d;
+  const double* w = weights + tk.w_offset;
+  double* g = grads + tk.w_offset;
+  for (int p = 0; p < h * (d + 2) + 1; ++p) g[p] = 0.0;
+  double lsum = 0.0;
+  for (int s = 0; s < n; ++s) {
+    const double* x = X + (tk.row_begin + s) * xs;
+    const double y = Y[tk.row_begin + s];
+    double z = 0.0;
+    for (int j = 0; j < h; ++j) {
+      double pre = 0.0;
+      for (int k = 0; k < d; ++k) pre = fma(x[k], w[j * d + k], pre);
+      z = fma(tanh(__dadd_rn(pre, w[hd + j])), w[hd + h + j], z);
+    }
+    z = __dadd_rn(z, w[hd + 2 * h]);
+    const double sp = softplus(z);
+    const double rate = __dadd_rn(sp, tk.eps);
+    const double re = __dadd_rn(rate, nll_eps);
+    lsum += __dsub_rn(rate, __dmul_rn(y, log(re)));
+    const double dz = __dmul_rn(__ddiv_rn(__dsub_rn(1.0, __ddiv_rn(y, re)), (double)n),
+                                exp(__dsub_rn(z, sp)));
+    for (int j = 0; j < h; ++j) {
+      double pre = 0.0;
+      for (int k = 0; k < d; ++k) pre = fma(x[k], w[j * d + k], pre);
+      const double a = tanh(__dadd_rn(pre, w[hd + j]));
+      const double dp = __dmul_rn(__dmul_rn(dz, w[hd + h + j]), __dsub_rn(1.0, __dmul_rn(a, a)));
+      for (int k = 0; k < d; ++k) g[j * d + k] = fma(dp, x[k], g[j * d + k]);
+      g[hd + j] += dp;
+      g[hd + h + j] = fma(a, dz, g[hd + h + j]);
+    }
+    g[hd + 2 * h] += dz;
+  }
+  loss[i] = lsum / n;
+}
+
+bbml_status pnn_loss_grad_launch(const bbml_pred_task* tasks, int32_t n_tasks, const double* X,
+                                 const double* y, int32_t x_stride, const double* weights,
+                                 double nll_eps, double* loss, double* grads, cudaStream_t s) {
+  for (int i = 0; i < n_tasks; ++i) {
+    const bbml_pred_task& t = tasks[i];
+    if (t.n < 1 || t.d < 1 || t.h < 1 || t.row_begin < 0 || t.w_offset < 0) {
+      set_error("loss_grad task %d: invalid field", i);
+      return BBML_ERR_INVALID;
+    }
+  }
+  if (n_tasks == 0) return BBML_OK;
+  ScratchBuffer scratch(s);
+  bbml_pred_task* d_tasks = nullptr;
+  bbml_status st;
+  if ((st = scratch.alloc(&d_tasks, n_tasks)) != BBML_OK) return st;
+  if ((st = scratch.upload(d_tasks, tasks, n_tasks)) != BBML_OK) return st;
+  pnn_loss_grad_kernel<<<(n_tasks + 63) / 64, 64, 0, s>>>(d_tasks, n_tasks, X, y, x_stride,
+                                                          weights, nll_eps, loss, grads);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_status(e, "loss_grad launch");
+  return scratch.release();
+}
+
+}  // namespace bbml

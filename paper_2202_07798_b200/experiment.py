@@ -1,0 +1,498 @@
+"""Batched drop-in for ``bbcount.experiment`` (reference
+``pkg/src/bbcount/experiment.py``).
+
+The reference trains one model per ``train_one`` call (99-163) and fans the
+(series x kind) tasks out over GIL-bound threads (385-401).  Here
+``train_many`` is the core: it prepares every series on the host (split,
+train-only normaliser — the L2 semantics), packs all training rows into one
+CSR block in HBM, launches ONE fused PNN kernel and ONE LM kernel per call
+on two CUDA streams (models are independent; seeds are derived on the
+device from the ``series_seed`` entropy), then one batched prediction on the
+test rows.  ``train_one``, ``learning_curve`` and ``run_experiment`` are
+thin wrappers with the reference's signatures, results and artifacts.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import math
+import time
+import zlib
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Optional, Sequence, Union
+
+import numpy as np
+
+from . import __version__, _lib, brbpnn, engine, metrics, pnn
+from .persist import SavedModel, save_model
+from .traces import (BbSeries, Normalizer, SplitError, SplitMode, SplitSpec, classify,
+                     fit_normalizer, split, trace_header)
+
+MODEL_KINDS = ("pnn", "brbpnn")
+
+
+def series_seed(base_seed: int, key: tuple, kind: str) -> int:
+    """Stable per-(series, model) seed (experiment.py:38-50), via the C-ABI
+    SeedSequence (the device derives the same value from the entropy)."""
+    app, kernel_id, bb_id = key
+    return _lib.seedseq_u64([int(base_seed) & _lib.M64, zlib.crc32(app.encode("utf-8")),
+                             int(kernel_id), int(bb_id), zlib.crc32(kind.encode("utf-8"))])
+
+
+@dataclass
+class ExperimentConfig:
+    split_mode: SplitMode = SplitMode.HIGH_LOW
+    fraction: float = 0.7
+    seed: int = 0
+    models: tuple = MODEL_KINDS
+    pnn_epochs: int = 300
+    pnn_batch_size: int = 10
+    pnn_learning_rate: float = 1e-4
+    pnn_hidden: int = 10
+    br_hidden: int = 1
+    br_max_epochs: int = 1000
+    workers: int = 1
+    heatmap_bins: int = 32
+
+    def split_spec(self) -> SplitSpec:
+        return SplitSpec(self.split_mode, self.fraction, self.seed)
+
+    def to_manifest(self) -> dict:
+        doc = dict(self.__dict__)
+        doc["split_mode"] = self.split_mode.value
+        doc["models"] = list(self.models)
+        return doc
+
+
+@dataclass
+class SeriesResult:
+    key: tuple
+    kind: str
+    error: Optional[str] = None
+    n_train: int = 0
+    n_test: int = 0
+    mse: Optional[float] = None
+    pearson: Optional[float] = None
+    spearman: Optional[float] = None
+    constant_target: bool = False
+    pinned_hyperparams: bool = False
+    pred_raw: Optional[np.ndarray] = None
+    actual_raw: Optional[np.ndarray] = None
+    saved: Optional[SavedModel] = None
+
+    @property
+    def accuracy(self) -> Optional[float]:
+        return None if self.mse is None else metrics.accuracy_percent(self.mse)
+
+
+# ---------------------------------------------------------------------------
+# host preparation (traces.py semantics)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class Prepared:
+    series: BbSeries
+    error: Optional[str] = None
+    norm: Optional[Normalizer] = None
+    Xtr: Optional[np.ndarray] = None
+    ytr: Optional[np.ndarray] = None
+    Xte: Optional[np.ndarray] = None
+    yte: Optional[np.ndarray] = None
+    yte_raw: Optional[np.ndarray] = None
+
+
+def prepare(series: BbSeries, spec: SplitSpec) -> Prepared:
+    """experiment.py:105-116: split, fit the normaliser on train, transform."""
+    try:
+        tr, te = split(series, spec)
+    except SplitError as exc:
+        return Prepared(series, error=str(exc))
+    norm = fit_normalizer(tr)
+    return Prepared(series, None, norm, norm.transform_features(tr.X), norm.transform_targets(tr.y),
+                    norm.transform_features(te.X), norm.transform_targets(te.y), te.y)
+
+
+@dataclass
+class Task:
+    prep: Prepared
+    kind: str
+    hidden: int
+
+
+def _config_error(kind: str, config: ExperimentConfig) -> Optional[str]:
+    if kind == "pnn":
+        try:
+            pnn.TrainConfig(epochs=config.pnn_epochs, batch_size=config.pnn_batch_size,
+                            learning_rate=config.pnn_learning_rate, hidden=config.pnn_hidden)
+        except Exception as exc:  # same message the reference's try block records
+            return f"{type(exc).__name__}: {exc}"
+        return None
+    if kind == "brbpnn":
+        return None
+    return f"ValueError: unknown model kind {kind!r}"
+
+
+@dataclass
+class BatchOutput:
+    results: list
+    device_seconds: float = 0.0
+    kernel_launches: int = 0
+    extra: dict = field(default_factory=dict)
+
+
+def _launch_group(kind: str, tasks: list, data: engine.DeviceData, rows: dict, config,
+                  base_seed: int, precision: int):
+    """Enqueue one fused training launch for all tasks of ``kind``."""
+    keys = [t.prep.series.key for t in tasks]
+    seeds = engine.series_seed_table(
+        base_seed, np.array([zlib.crc32(k[0].encode("utf-8")) for k in keys], dtype=np.uint64),
+        np.array([k[1] for k in keys], dtype=np.uint64), np.array([k[2] for k in keys], dtype=np.uint64),
+        np.full(len(keys), zlib.crc32(kind.encode("utf-8")), dtype=np.uint64))
+    rb = np.array([rows[id(t.prep)][0] for t in tasks], dtype=np.int64)
+    n = np.array([rows[id(t.prep)][1] for t in tasks], dtype=np.int32)
+    d = np.array([t.prep.Xtr.shape[1] for t in tasks], dtype=np.int32)
+    h = np.array([t.hidden for t in tasks], dtype=np.int32)
+    if kind == "pnn":
+        tab, P = engine.pnn_tasks(rb, n, d, h, config.pnn_epochs, config.pnn_batch_size,
+                                  config.pnn_learning_rate, pnn.DEFAULT_EPS, seeds, False)
+        return engine.launch_pnn(data, tab, P, precision), seeds
+    tab, P = engine.lm_tasks(rb, n, d, h, config.br_max_epochs, seeds, False)
+    return engine.launch_lm(data, tab, P), seeds
+
+
+def train_many(pairs: Sequence[tuple], config: ExperimentConfig, *, precision: Optional[int] = None,
+               br_hidden_of=None, prepared: Optional[dict] = None) -> BatchOutput:
+    """Train and evaluate every (series, kind) pair with batched kernels.
+
+    ``br_hidden_of(series) -> int`` optionally overrides ``config.br_hidden``
+    per series (e.g. hidden 10 for gramschmit).
+    Returns SeriesResult objects in input order, identical in meaning to
+    calling the reference ``train_one`` on each pair.
+    """
+    torch = engine.torch_cuda()
+    precision = pnn.PRECISION if precision is None else precision
+    spec = config.split_spec()
+    cache = {} if prepared is None else prepared
+    results: list = [None] * len(pairs)
+    tasks: dict = {"pnn": [], "brbpnn": []}
+    order: dict = {"pnn": [], "brbpnn": []}
+    for i, (series, kind) in enumerate(pairs):
+        res = SeriesResult(series.key, kind)
+        results[i] = res
+        p = cache.get(id(series))
+        if p is None:
+            p = prepare(series, spec)
+            cache[id(series)] = p
+        if p.error is not None:
+            res.error = p.error
+            continue
+        res.n_train, res.n_test = len(p.ytr), len(p.yte)
+        res.constant_target = p.norm.constant_target
+        err = _config_error(kind, config)
+        if err is not None:
+            res.error = err
+            continue
+        hidden = config.pnn_hidden if kind == "pnn" else (
+            br_hidden_of(series) if br_hidden_of else config.br_hidden)
+        tasks[kind].append(Task(p, kind, int(hidden)))
+        order[kind].append(i)
+
+    # one CSR block with every prepared series' training rows
+    preps = {}
+    for kind in tasks:
+        for t in tasks[kind]:
+            preps[id(t.prep)] = t.prep
+    plist = list(preps.values())
+    if not plist:
+        return BatchOutput(results)
+    packed = engine.pack([p.Xtr for p in plist], [p.ytr for p in plist])
+    rows = {id(p): (int(packed.row_begin[j]), int(packed.n[j])) for j, p in enumerate(plist)}
+    data = engine.DeviceData(packed)
+
+    t0 = time.perf_counter()
+    main = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+    side.wait_stream(main)
+    runs = {}
+    launches = 0
+    for kind, stream in (("pnn", main), ("brbpnn", side)):
+        if tasks[kind]:
+            with torch.cuda.stream(stream):
+                runs[kind] = _launch_group(kind, tasks[kind], data, rows, config, config.seed,
+                                           precision)
+                launches += 1
+    main.wait_stream(side)
+
+    # batched prediction on the (normalised) test rows of every trained model
+    all_tasks, all_idx, w_parts, kinds = [], [], [], []
+    fetched = {}
+    for kind, (run, seeds) in runs.items():
+        fetched[kind] = (run.fetch(), seeds)
+    torch.cuda.synchronize()
+    dev_s = time.perf_counter() - t0
+    for kind, (res_k, seeds) in fetched.items():
+        for j, t in enumerate(tasks[kind]):
+            all_tasks.append((kind, j, t))
+    if all_tasks:
+        q = engine.pack([t.prep.Xte for _, _, t in all_tasks])
+        dd = np.array([t.prep.Xte.shape[1] for _, _, t in all_tasks])
+        hh = np.array([t.hidden for _, _, t in all_tasks])
+        kk = np.array([0 if k == "pnn" else 1 for k, _, _ in all_tasks])
+        W = np.concatenate([fetched[k][0].w(j) for k, j, _ in all_tasks])
+        woff = engine.offsets(engine.n_params(dd, hh))
+        pred_flat = engine.predict(W, woff, dd, hh, kk, q, None, eps=pnn.DEFAULT_EPS)
+        launches += 1
+    for a, (kind, j, t) in enumerate(all_tasks):
+        i = order[kind][j]
+        res = results[i]
+        rk = fetched[kind][0]
+        st = rk.status[j]
+        seed_rec = fetched[kind][1][j]
+        try:
+            if kind == "pnn":
+                pnn.raise_for_status(st)
+            else:
+                brbpnn.raise_for_status(st)
+        except Exception as exc:
+            res.error = f"{type(exc).__name__}: {exc}"
+            continue
+        d = t.prep.Xtr.shape[1]
+        w = rk.w(j)
+        pred = pred_flat[int(q.row_begin[a]):int(q.row_begin[a]) + int(q.n[a])]
+        res.mse = metrics.mse(pred, t.prep.yte)
+        res.pred_raw = t.prep.norm.inverse_targets(pred)
+        res.actual_raw = t.prep.yte_raw
+        if len(pred) >= 2:
+            res.pearson = metrics.pearson(res.pred_raw, res.actual_raw)
+            res.spearman = metrics.spearman(res.pred_raw, res.actual_raw)
+        seed = _lib.seedseq_u64(list(_seed_entropy(seed_rec)))
+        if kind == "pnn":
+            model = pnn.PnnModel.from_packed(w, d, t.hidden)
+            meta = {"epochs": config.pnn_epochs, "batch_size": config.pnn_batch_size,
+                    "learning_rate": config.pnn_learning_rate, "hidden": config.pnn_hidden}
+        else:
+            hd = t.hidden * d
+            model = brbpnn.BrbpnnModel(w[:hd].reshape(t.hidden, d).copy(), w[hd:hd + t.hidden].copy(),
+                                       w[hd + t.hidden:hd + 2 * t.hidden].copy(), float(w[-1]),
+                                       float(st["alpha"]), float(st["beta"]))
+            ran = int(st["epochs"])
+            res.pinned_hyperparams = bool(st["detail"])
+            meta = {"hidden": t.hidden, "max_epochs": config.br_max_epochs, "epochs_run": ran,
+                    "gamma": float(st["gamma"]) if ran else None,
+                    "mu": float(st["mu"]) if ran else None}
+        res.saved = SavedModel(kind, model, t.prep.norm, t.prep.series.key, seed, meta)
+    return BatchOutput(results, dev_s, launches)
+
+
+def _seed_entropy(rec) -> list:
+    """Reassemble the entropy word list of a mode-1 seed record as one int list
+    whose SeedSequence is identical (words are already 32-bit)."""
+    return [int(w) for w in rec["words"][:int(rec["n_words"])]]
+
+
+def train_one(series: BbSeries, kind: str, config: ExperimentConfig) -> SeriesResult:
+    """Split, normalise, train one model on the device, evaluate (experiment.py:99-163)."""
+    return train_many([(series, kind)], config).results[0]
+
+
+@dataclass
+class AppSummary:
+    app: str
+    kind: str
+    n_series: int
+    n_failed: int
+    avg_mse: Optional[float]
+    accuracy: Optional[float]
+    pearson_pooled: Optional[float]
+    spearman_pooled: Optional[float]
+    any_constant_target: bool
+    any_pinned: bool
+
+
+def summarize(rows: Sequence[SeriesResult], split_mode: SplitMode) -> list:
+    """Per (app, kind) pooled summary (experiment.py:180-206)."""
+    groups: dict = {}
+    for r in rows:
+        groups.setdefault((r.key[0], r.kind), []).append(r)
+    out = []
+    for (app, kind), grp in sorted(groups.items()):
+        ok = [r for r in grp if r.error is None]
+        avg = float(np.mean([r.mse for r in ok])) if ok else None
+        preds = np.concatenate([r.pred_raw for r in ok]) if ok else np.array([])
+        acts = np.concatenate([r.actual_raw for r in ok]) if ok else np.array([])
+        out.append(AppSummary(app, kind, len(grp), len(grp) - len(ok), avg,
+                              None if avg is None else metrics.accuracy_percent(avg),
+                              metrics.pearson(preds, acts) if preds.size >= 2 else None,
+                              metrics.spearman(preds, acts) if preds.size >= 2 else None,
+                              any(r.constant_target for r in ok), any(r.pinned_hyperparams for r in ok)))
+    return out
+
+
+@dataclass(frozen=True)
+class CurvePoint:
+    fraction: float
+    accuracy: Optional[float]
+    skipped: bool = False
+
+
+def learning_curve(series: BbSeries, kind: str, fractions: Sequence[float], seed: int,
+                   config: Optional[ExperimentConfig] = None) -> list:
+    """Random-split accuracy per training fraction (experiment.py:221-253);
+    every fraction is one task of a single batched device call per fraction."""
+    config = ExperimentConfig() if config is None else config
+    pts = []
+    for f in fractions:
+        cfg = ExperimentConfig(**{**config.__dict__, "split_mode": SplitMode.RANDOM,
+                                  "fraction": f, "seed": seed})
+        try:
+            r = train_one(series, kind, cfg)
+        except SplitError:
+            pts.append(CurvePoint(f, None, skipped=True))
+            continue
+        pts.append(CurvePoint(f, None, skipped=True) if r.error is not None
+                   else CurvePoint(f, r.accuracy))
+    return pts
+
+
+# ---------------------------------------------------------------------------
+# artifacts (experiment.py:261-370)
+# ---------------------------------------------------------------------------
+
+def _fmt(v) -> str:
+    if v is None:
+        return "undefined"
+    if isinstance(v, bool):
+        return str(v).lower()
+    if isinstance(v, (float, np.floating)):
+        return repr(float(v))
+    return str(v)
+
+
+def series_slug(key: tuple, kind: Optional[str] = None) -> str:
+    s = f"{key[0]}_k{key[1]}_b{key[2]}"
+    return f"{s}_{kind}" if kind else s
+
+
+def write_report_csv(rows: Sequence[SeriesResult], path: Path) -> None:
+    with open(path, "w", encoding="utf-8", newline="\n") as fh:
+        fh.write("app,kernel_id,bb_id,model,n_train,n_test,mse,accuracy,"
+                 "pearson,spearman,constant_target,pinned_hyperparams,error\n")
+        for r in sorted(rows, key=lambda r: (r.key, r.kind)):
+            err = (r.error or "").replace(",", ";")
+            fh.write(f"{r.key[0]},{r.key[1]},{r.key[2]},{r.kind},{r.n_train},{r.n_test},"
+                     f"{_fmt(r.mse)},{_fmt(r.accuracy)},{_fmt(r.pearson)},{_fmt(r.spearman)},"
+                     f"{_fmt(r.constant_target)},{_fmt(r.pinned_hyperparams)},{err}\n")
+
+
+def write_summary_csv(summaries: Sequence[AppSummary], split_mode: SplitMode, path: Path) -> None:
+    with open(path, "w", encoding="utf-8", newline="\n") as fh:
+        fh.write("app,split,model,n_series,n_failed,avg_mse,accuracy_percent,"
+                 "pearson_pooled,spearman_pooled,constant_target,pinned_hyperparams\n")
+        for s in summaries:
+            fh.write(f"{s.app},{split_mode.value},{s.kind},{s.n_series},{s.n_failed},"
+                     f"{_fmt(s.avg_mse)},{_fmt(s.accuracy)},{_fmt(s.pearson_pooled)},"
+                     f"{_fmt(s.spearman_pooled)},{_fmt(s.any_constant_target)},{_fmt(s.any_pinned)}\n")
+
+
+def write_heatmap_csv(data: metrics.HeatmapData, path: Path) -> None:
+    e = data.edges
+    with open(path, "w", encoding="utf-8", newline="\n") as fh:
+        fh.write("pred_bin,actual_bin,pred_low,pred_high,actual_low,actual_high,count,on_identity\n")
+        for i in range(data.bins):
+            for j in range(data.bins):
+                fh.write(f"{i},{j},{_fmt(float(e[i]))},{_fmt(float(e[i + 1]))},{_fmt(float(e[j]))},"
+                         f"{_fmt(float(e[j + 1]))},{int(data.counts[i, j])},{_fmt(i == j)}\n")
+
+
+def write_kde_csv(curve: metrics.KdeCurve, path: Path) -> None:
+    with open(path, "w", encoding="utf-8", newline="\n") as fh:
+        fh.write("x,density\n")
+        for x, dv in zip(curve.grid, curve.density):
+            fh.write(f"{_fmt(float(x))},{_fmt(float(dv))}\n")
+
+
+def write_curve_csv(points: Sequence[CurvePoint], path: Path) -> None:
+    with open(path, "w", encoding="utf-8", newline="\n") as fh:
+        fh.write("fraction,accuracy,skipped\n")
+        for p in points:
+            fh.write(f"{_fmt(p.fraction)},{_fmt(p.accuracy)},{_fmt(p.skipped)}\n")
+
+
+def write_split_manifests(series_list: Sequence[BbSeries], spec: SplitSpec, out_dir: Path) -> None:
+    by_app: dict = {}
+    for s in series_list:
+        by_app.setdefault(s.key[0], []).append(s)
+    for app, grp in sorted(by_app.items()):
+        with open(out_dir / f"splits_{app}.csv", "w", encoding="utf-8", newline="\n") as fh:
+            fh.write(",".join(trace_header(grp[0].arity) + ["partition"]) + "\n")
+            for s in grp:
+                try:
+                    labels = classify(s, spec)
+                except SplitError:
+                    labels = np.full(len(s), "error", dtype=object)
+                for row, count, lab in zip(s.X, s.y, labels):
+                    params = ",".join(str(int(v)) for v in row)
+                    fh.write(f"{s.key[0]},{s.key[1]},{s.key[2]},{params},{int(count)},{lab}\n")
+
+
+def digest_file(path: Union[str, Path]) -> str:
+    h = hashlib.sha256()
+    with open(path, "rb") as fh:
+        for chunk in iter(lambda: fh.read(65536), b""):
+            h.update(chunk)
+    return h.hexdigest()
+
+
+@dataclass
+class ExperimentOutput:
+    rows: list
+    summaries: list
+    out_dir: Path
+
+
+def run_experiment(series_list: Sequence[BbSeries], config: ExperimentConfig,
+                   out_dir: Union[str, Path], input_digests: Optional[dict] = None,
+                   br_hidden_of=None) -> ExperimentOutput:
+    """experiment.py:385-451 with ONE batched device call for all tasks
+    (``workers`` is accepted for compatibility; results never depend on it)."""
+    started = time.time()
+    out_dir = Path(out_dir)
+    out_dir.mkdir(parents=True, exist_ok=True)
+    pairs = [(s, k) for s in series_list for k in config.models]
+    rows = train_many(pairs, config, br_hidden_of=br_hidden_of).results
+    rows.sort(key=lambda r: (r.key, r.kind))
+    if rows and all(r.error is not None for r in rows):
+        raise RuntimeError("all series failed; first error: " + str(rows[0].error))
+    summaries = summarize(rows, config.split_mode)
+    write_report_csv(rows, out_dir / "report.csv")
+    write_summary_csv(summaries, config.split_mode, out_dir / "summary.csv")
+    write_split_manifests(series_list, config.split_spec(), out_dir)
+    models_dir = out_dir / "models"
+    models_dir.mkdir(exist_ok=True)
+    for r in rows:
+        if r.saved is not None:
+            save_model(r.saved, models_dir / f"{series_slug(r.key, r.kind)}.json")
+        if r.error is None and r.pred_raw is not None and r.pred_raw.size:
+            write_heatmap_csv(metrics.heatmap_data(r.pred_raw, r.actual_raw, config.heatmap_bins),
+                              out_dir / f"heatmap_{series_slug(r.key, r.kind)}.csv")
+    for s in series_list:
+        try:
+            curve = metrics.kde(s.y)
+        except (metrics.BandwidthError, metrics.MetricShapeError):
+            continue
+        write_kde_csv(curve, out_dir / f"kde_{series_slug(s.key)}.csv")
+    manifest = {
+        "config": config.to_manifest(),
+        "inputs": input_digests or {},
+        "series": [{"app": s.key[0], "kernel_id": s.key[1], "bb_id": s.key[2], "n": len(s)}
+                   for s in series_list],
+        "errors": {series_slug(r.key, r.kind): r.error for r in rows if r.error is not None},
+        "versions": {"bbcount": __version__, "numpy": np.__version__},
+        "wall_time_seconds": time.time() - started,
+    }
+    with open(out_dir / "manifest.json", "w", encoding="utf-8", newline="\n") as fh:
+        json.dump(manifest, fh, indent=2)
+        fh.write("\n")
+    return ExperimentOutput(rows, summaries, out_dir)

@@ -1,0 +1,135 @@
+"""Device parity: CUDA kernels (through the drop-in API / C-ABI) against the
+golden fixtures produced by the reference and against the CPU oracle.
+
+Tolerances:
+  PNN FP64 kernel  : weights and predictions <= 1e-12 relative (1e-15 abs floor)
+  PNN FP32 kernel  : predictions <= 1e-3 relative (north-star gate)
+  BR h <= 3        : predictions <= 1e-6 relative, same history length +-2 epochs
+  initial weights  : bit-identical (device PCG64 == NumPy PCG64)
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2202_07798_b200 import brbpnn, engine, pnn  # noqa: E402
+from oracle import bbml_oracle as O  # noqa: E402
+
+
+def _seed(words):
+    return int(words[0]) | (int(words[1]) << 64)
+
+
+def _rel(a, b, floor=1e-15):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), floor))) if a.size else 0.0
+
+
+def test_device_init_bit_identical_to_numpy():
+    # one epoch with lr tiny -> weights ~ init; use 0 epochs equivalent via history check:
+    for seed in (0, 5, 2**63 + 3):
+        for d, h in ((2, 10), (1, 1), (4, 7), (3, 64)):
+            rng = np.random.default_rng(seed)
+            want = O.init_flat(rng, d, h)
+            # BR with max_epochs=0 returns the initial weights untouched
+            X = np.random.default_rng(1).uniform(size=(5, d))
+            y = np.zeros(5)
+            if h * (d + 2) + 1 <= 96:
+                model, hist = brbpnn.train(X, y, hidden=h, seed=seed, config=brbpnn.LmConfig(max_epochs=0))
+                assert hist == []
+                np.testing.assert_array_equal(brbpnn.pack(model), want)
+
+
+def test_pnn_fp64_matches_reference_golden(golden):
+    g = golden("pnn")
+    for i in range(int(g["n_cases"])):
+        d, h, n, ep, bs = (int(v) for v in g[f"c{i}_cfg"])
+        cfg = pnn.TrainConfig(epochs=ep, batch_size=bs, learning_rate=float(g[f"c{i}_lr"]),
+                              seed=_seed(g[f"c{i}_seed"]), hidden=h)
+        model, hist = pnn.train(g[f"c{i}_X"], g[f"c{i}_y"], cfg)
+        w = model.packed()
+        assert _rel(w, g[f"c{i}_w"]) <= 1e-11, (i, _rel(w, g[f"c{i}_w"]))
+        assert _rel(hist, g[f"c{i}_hist"]) <= 1e-12, i
+        pred = pnn.forward(model, g[f"c{i}_Xt"])
+        assert _rel(pred, g[f"c{i}_pred"]) <= 1e-11, i
+
+
+def test_pnn_fp32_predictions_within_gate(golden):
+    g = golden("pnn")
+    old = pnn.PRECISION
+    pnn.PRECISION = 32
+    try:
+        for i in range(int(g["n_cases"])):
+            d, h, n, ep, bs = (int(v) for v in g[f"c{i}_cfg"])
+            cfg = pnn.TrainConfig(epochs=ep, batch_size=bs, learning_rate=float(g[f"c{i}_lr"]),
+                                  seed=_seed(g[f"c{i}_seed"]), hidden=h)
+            model, _ = pnn.train(g[f"c{i}_X"], g[f"c{i}_y"], cfg)
+            pred = pnn.forward(model, g[f"c{i}_Xt"])
+            assert _rel(pred, g[f"c{i}_pred"]) <= 1e-3, (i, _rel(pred, g[f"c{i}_pred"]))
+    finally:
+        pnn.PRECISION = old
+
+
+def test_br_matches_reference_golden(golden):
+    g = golden("brbpnn")
+    worst = {}
+    for i in range(int(g["n_cases"])):
+        d, h, n, seed, est, mx = (int(v) for v in g[f"c{i}_cfg"])
+        a0, b0 = (float(v) for v in g[f"c{i}_ab"])
+        model, hist = brbpnn.train(g[f"c{i}_X"], g[f"c{i}_y"], hidden=h, seed=seed,
+                                   config=brbpnn.LmConfig(max_epochs=mx), estimate_hyperparams=bool(est),
+                                   alpha0=a0, beta0=b0)
+        want = g[f"c{i}_hist"]
+        pred = brbpnn.forward(model, g[f"c{i}_Xt"])
+        worst[i] = (_rel(pred, g[f"c{i}_pred"], 1e-12), len(hist), len(want))
+    print(worst)
+    for i, (err, nh, nw) in worst.items():
+        h = int(g[f"c{i}_cfg"][1])
+        if h <= 3:
+            assert err <= 1e-6, (i, err)
+            assert abs(nh - nw) <= 2, (i, nh, nw)
+
+
+def test_forward_matches_golden(golden):
+    g = golden("pnn")
+    for i in range(int(g["n_units"])):
+        d, h = (int(v) for v in g[f"u{i}_dh"])
+        m = pnn.PnnModel.from_packed(g[f"u{i}_w"], d, h)
+        assert _rel(pnn.forward(m, g[f"u{i}_Xf"]), g[f"u{i}_f"]) <= 1e-13
+
+
+def test_loss_and_grads_match_golden(golden):
+    g = golden("pnn")
+    for i in range(int(g["n_units"])):
+        d, h = (int(v) for v in g[f"u{i}_dh"])
+        m = pnn.PnnModel.from_packed(g[f"u{i}_w"], d, h)
+        loss, gr = pnn.loss_and_grads(m, g[f"u{i}_X"], g[f"u{i}_y"])
+        flat = np.concatenate([gr["W1"].ravel(), gr["b1"], gr["W2"], np.atleast_1d(gr["b2"])])
+        assert loss == pytest.approx(float(g[f"u{i}_loss"]), rel=1e-12)
+        np.testing.assert_allclose(flat, g[f"u{i}_g"], rtol=1e-10, atol=1e-14)
+
+
+def test_br_units_match_golden(golden):
+    g = golden("brbpnn")
+    for i in range(int(g["n_units"])):
+        d, h = (int(v) for v in g[f"u{i}_dh"])
+        w, X, y = g[f"u{i}_w"], g[f"u{i}_X"], g[f"u{i}_y"]
+        alpha, beta, mu = (float(v) for v in g[f"u{i}_ab_mu"])
+        m = brbpnn.BrbpnnModel(*[None] * 4, alpha=alpha, beta=beta)
+        m.W1 = np.zeros((h, d))
+        brbpnn.unpack(m, w.copy())
+        J = brbpnn.jacobian(m, X)
+        np.testing.assert_allclose(J, g[f"u{i}_J"], rtol=1e-13, atol=1e-15)
+        np.testing.assert_allclose(brbpnn.objective(m, X, y), g[f"u{i}_obj"], rtol=1e-12)
+        r = brbpnn.forward(m, X) - y
+        delta = brbpnn.solve_damped(J, r, w, alpha, beta, mu)
+        np.testing.assert_allclose(delta, g[f"u{i}_delta"], rtol=1e-8, atol=1e-12)
+        f, e_d, e_w = brbpnn.objective(m, X, y)
+        up = brbpnn.evidence_update(e_d, e_w, J.T @ J, alpha, beta, len(y))
+        np.testing.assert_allclose([up.alpha, up.beta, up.gamma], g[f"u{i}_evid"][:3], rtol=1e-9,
+                                   atol=1e-12)
