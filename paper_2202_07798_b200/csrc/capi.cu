@@ -24,6 +24,48 @@ bbml_status cuda_status(cudaError_t e, const char* what) {
   return BBML_ERR_CUDA;
 }
 
+namespace {
+struct ForkPool {
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> events;
+  cudaEvent_t fork = nullptr;
+};
+thread_local std::vector<ForkPool> g_pools;  // per device, per host thread
+}  // namespace
+
+StreamFork::StreamFork(cudaStream_t parent, int n) : parent_(parent), n_(n) {
+  if (n_ <= 1) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if ((int)g_pools.size() <= dev) g_pools.resize(dev + 1);
+  ForkPool& p = g_pools[dev];
+  if (!p.fork) cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming);
+  while ((int)p.streams.size() < n_) {
+    cudaStream_t s;
+    cudaEvent_t e;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    p.streams.push_back(s);
+    p.events.push_back(e);
+  }
+  cudaEventRecord(p.fork, parent_);
+  for (int i = 0; i < n_; ++i) {
+    cudaStreamWaitEvent(p.streams[i], p.fork, 0);
+    kids_.push_back(p.streams[i]);
+    done_.push_back(p.events[i]);
+  }
+}
+
+bbml_status StreamFork::join() {
+  if (n_ <= 1) return BBML_OK;
+  for (int i = 0; i < n_; ++i) {
+    cudaEventRecord(done_[i], kids_[i]);
+    cudaStreamWaitEvent(parent_, done_[i], 0);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BBML_OK : cuda_status(e, "stream fork/join");
+}
+
 bbml_status pnn_loss_grad_launch(const bbml_pred_task*, int32_t, const double*, const double*,
                                  int32_t, const double*, double, double*, double*, cudaStream_t);
 bbml_status lm_jacobian_launch(const bbml_pred_task*, int32_t, const double*, const double*,

@@ -81,6 +81,23 @@ class ScratchBuffer {
   std::vector<void*> ptrs_;
 };
 
+// Fork/join of the caller's stream so the independent per-shape launches of
+// one call (e.g. hidden-1 and hidden-10 LM buckets) run concurrently instead
+// of back to back.  Child streams/events come from a per-thread, per-device
+// pool created on first use (non-blocking streams, timing-disabled events).
+class StreamFork {
+ public:
+  StreamFork(cudaStream_t parent, int n);
+  cudaStream_t child(int i) const { return n_ > 1 ? kids_[i] : parent_; }
+  bbml_status join();
+
+ private:
+  cudaStream_t parent_;
+  int n_;
+  std::vector<cudaStream_t> kids_;
+  std::vector<cudaEvent_t> done_;
+};
+
 bbml_status pnn_train_launch(const bbml_pnn_task* tasks, int32_t n_tasks, const double* X,
                              const double* y, int32_t x_stride, double* weights, double* history,
                              bbml_model_status* status, int32_t precision, cudaStream_t stream);

@@ -458,6 +458,583 @@ __global__ void __launch_bounds__(LM_NT) lm_train_kernel(LmLaunch L) {
   }
 }
 
+// ===========================================================================
+// Warp-per-model LM trainer for P <= 32 (all hidden-1 models, and hidden 10
+// at d = 1, e.g. gramschmit): no block barriers at all.  Lanes stride over
+// samples for the energy / Jacobian passes.  Hidden-1 models (the paper's
+// default) use a compile-time-shaped path: weights, the
+// Jacobian row and the 1/2 P(P+1) + P accumulators of J'J | J'r live in
+// registers.  Other shapes stage 32 Jacobian rows in shared memory and
+// contract them lane-parallel.  LU with partial pivoting and the cyclic
+// Jacobi eigen-solver run lane-parallel on a per-warp shared-memory copy
+// (odd row stride: conflict-free column access), synchronised with
+// __syncwarp only.
+// ===========================================================================
+template <int PM>
+struct WarpLm {
+  static constexpr int LD = PM + 1;
+  static constexpr int NE = PM * (PM + 1) / 2 + PM;
+  double w[PM], wt[PM], delta[PM], jtr[PM], rhs[PM];
+  double jtj[PM * LD];
+  double A[PM * LD];
+  static constexpr int JCH = PM > 8 ? 8 : 32;  // staged Jacobian rows per chunk
+  double Jc[JCH * PM];
+  double rc[JCH];
+  double cs[2 * 16];
+  int pq[16];
+  unsigned short ent[NE];  // (a << 8 | b) for the upper triangle, b == P -> J'r
+  unsigned short rr[(PM > 1 ? PM - 1 : 1) * (PM / 2)];  // round-robin pair schedule (p | q << 8)
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  return v;
+}
+
+// hidden-1 model with D inputs, pack order [W1 (D), b1, W2, b2]
+template <int D>
+struct H1 {
+  double w1[D], b1, w2, b2;
+  __device__ __forceinline__ void load(const double* w) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) w1[k] = w[k];
+    b1 = w[D];
+    w2 = w[D + 1];
+    b2 = w[D + 2];
+  }
+  // forward exactly as br_sample: dot, + b1, tansig, a*w2 (+0), + b2
+  __device__ __forceinline__ double out(const double (&x)[D], double& a) const {
+    double pre = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) pre = fma(x[k], w1[k], pre);
+    a = tansig(__dadd_rn(pre, b1));
+    return __dadd_rn(fma(a, w2, 0.0), b2);
+  }
+};
+
+template <int D>
+__device__ __forceinline__ void load_x(double (&x)[D], const double* X, int64_t i, int xs) {
+#pragma unroll
+  for (int k = 0; k < D; ++k) x[k] = __ldg(X + i * xs + k);
+}
+
+template <int PM, int D>
+__device__ double w_energy(const WarpLm<PM>& S, const double* wv, const double* X, const double* Y,
+                           int n, int d, int h, int xs, int lane) {
+  double acc = 0.0;
+  if constexpr (D > 0) {
+    H1<D> m;
+    m.load(wv);
+    // 4 samples per lane per iteration: independent exp/div chains (ILP);
+    // the accumulation order stays the sample order of the lane
+    constexpr int U4 = 4;
+    int i = lane;
+    for (; i + 32 * (U4 - 1) < n; i += 32 * U4) {
+      double r[U4];
+#pragma unroll
+      for (int u = 0; u < U4; ++u) {
+        double x[D];
+        load_x<D>(x, X, i + 32 * u, xs);
+        double a;
+        r[u] = __dsub_rn(m.out(x, a), __ldg(Y + i + 32 * u));
+      }
+#pragma unroll
+      for (int u = 0; u < U4; ++u) acc = fma(r[u], r[u], acc);
+    }
+    for (; i < n; i += 32) {
+      double x[D];
+      load_x<D>(x, X, i, xs);
+      double a;
+      const double r = __dsub_rn(m.out(x, a), __ldg(Y + i));
+      acc = fma(r, r, acc);
+    }
+  } else {
+    double x[BBML_MAX_INPUTS];
+    for (int i = lane; i < n; i += 32) {
+      for (int k = 0; k < d; ++k) x[k] = __ldg(X + (int64_t)i * xs + k);
+      const double r = __dsub_rn(br_sample(wv, x, d, h, nullptr), __ldg(Y + i));
+      acc = fma(r, r, acc);
+    }
+  }
+  return warp_sum(acc);
+}
+
+template <int PM, int D>
+__device__ void w_stats(WarpLm<PM>& S, const double* X, const double* Y, int n, int d, int h, int P,
+                        int xs, int lane) {
+  constexpr int LD = WarpLm<PM>::LD;
+  if constexpr (D > 0) {
+    constexpr int PP = D + 3;
+    constexpr int NA = PP * (PP + 1) / 2 + PP;
+    H1<D> m;
+    m.load(S.w);
+    double acc[NA];
+#pragma unroll
+    for (int e = 0; e < NA; ++e) acc[e] = 0.0;
+    for (int i = lane; i < n; i += 32) {
+      double x[D];
+      load_x<D>(x, X, i, xs);
+      double a;
+      const double r = __dsub_rn(m.out(x, a), __ldg(Y + i));
+      const double g = __dmul_rn(__dsub_rn(1.0, __dmul_rn(a, a)), m.w2);
+      double jr[PP];
+#pragma unroll
+      for (int k = 0; k < D; ++k) jr[k] = __dmul_rn(g, x[k]);
+      jr[D] = g;
+      jr[D + 1] = a;
+      jr[D + 2] = 1.0;
+      int e = 0;
+#pragma unroll
+      for (int p = 0; p < PP; ++p)
+#pragma unroll
+        for (int q = p; q < PP; ++q, ++e) acc[e] = fma(jr[p], jr[q], acc[e]);
+#pragma unroll
+      for (int p = 0; p < PP; ++p, ++e) acc[e] = fma(jr[p], r, acc[e]);
+    }
+    int e = 0;
+#pragma unroll
+    for (int p = 0; p < PP; ++p)
+#pragma unroll
+      for (int q = p; q < PP; ++q, ++e) {
+        const double v = warp_sum(acc[e]);
+        if (lane == 0) {
+          S.jtj[p * LD + q] = v;
+          S.jtj[q * LD + p] = v;
+        }
+      }
+#pragma unroll
+    for (int p = 0; p < PP; ++p, ++e) {
+      const double v = warp_sum(acc[e]);
+      if (lane == 0) S.jtr[p] = v;
+    }
+  } else {
+    const int ne = P * (P + 1) / 2 + P;
+    double x[BBML_MAX_INPUTS];
+    for (int e = lane; e < PM * LD; e += 32) S.jtj[e] = 0.0;
+    for (int e = lane; e < PM; e += 32) S.jtr[e] = 0.0;
+    constexpr int JCH = WarpLm<PM>::JCH;
+    for (int base = 0; base < n; base += JCH) {
+      const int cnt = min(JCH, n - base);
+      if (lane < cnt) {
+        const int i = base + lane;
+        for (int k = 0; k < d; ++k) x[k] = __ldg(X + (int64_t)i * xs + k);
+        S.rc[lane] = __dsub_rn(br_sample(S.w, x, d, h, S.Jc + lane * PM), __ldg(Y + i));
+      }
+      __syncwarp();
+      for (int e = lane; e < ne; e += 32) {
+        const int a = S.ent[e] >> 8, b = S.ent[e] & 255;
+        double s = (b < P) ? S.jtj[a * LD + b] : S.jtr[a];
+        if (b < P) {
+          for (int c = 0; c < cnt; ++c) s = fma(S.Jc[c * PM + a], S.Jc[c * PM + b], s);
+          S.jtj[a * LD + b] = s;
+        } else {
+          for (int c = 0; c < cnt; ++c) s = fma(S.Jc[c * PM + a], S.rc[c], s);
+          S.jtr[a] = s;
+        }
+      }
+      __syncwarp();
+    }
+    for (int e = lane; e < ne; e += 32) {
+      const int a = S.ent[e] >> 8, b = S.ent[e] & 255;
+      if (b < P && a != b) S.jtj[b * LD + a] = S.jtj[a * LD + b];
+    }
+  }
+  __syncwarp();
+}
+
+// LU with partial pivoting (first maximal |pivot|, as idamax) + substitutions
+template <int PM>
+__device__ bool w_solve(WarpLm<PM>& S, int P, double alpha, double beta, double mu, int lane) {
+  constexpr int LD = WarpLm<PM>::LD;
+  const double damp = __dadd_rn(mu, alpha);
+  if (lane < P) {
+    for (int b = 0; b < P; ++b) {
+      const double v = __dmul_rn(beta, S.jtj[lane * LD + b]);
+      S.A[lane * LD + b] = (lane == b) ? __dadd_rn(v, damp) : v;
+    }
+    S.rhs[lane] = -__dadd_rn(__dmul_rn(beta, S.jtr[lane]), __dmul_rn(alpha, S.w[lane]));
+  }
+  __syncwarp();
+  for (int k = 0; k < P; ++k) {
+    double best = (lane >= k && lane < P) ? fabs(S.A[lane * LD + k]) : -1.0;
+    int bi = lane;
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, m);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, m);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    const int p = bi;
+    if (S.A[p * LD + k] == 0.0) return false;
+    if (p != k) {
+      if (lane < P) {
+        const double t = S.A[k * LD + lane];
+        S.A[k * LD + lane] = S.A[p * LD + lane];
+        S.A[p * LD + lane] = t;
+      }
+      if (lane == 0) {
+        const double t = S.rhs[k];
+        S.rhs[k] = S.rhs[p];
+        S.rhs[p] = t;
+      }
+    }
+    __syncwarp();
+    if (lane > k && lane < P) {
+      const double l = __ddiv_rn(S.A[lane * LD + k], S.A[k * LD + k]);
+      S.A[lane * LD + k] = l;
+      for (int j = k + 1; j < P; ++j) S.A[lane * LD + j] = fma(-l, S.A[k * LD + j], S.A[lane * LD + j]);
+    }
+    __syncwarp();
+  }
+  for (int i = 0; i < P; ++i) {
+    double s = 0.0;
+    for (int j = lane; j < i; j += 32) s = fma(S.A[i * LD + j], S.rhs[j], s);
+    s = warp_sum(s);
+    if (lane == 0) S.rhs[i] = __dsub_rn(S.rhs[i], s);
+    __syncwarp();
+  }
+  for (int i = P - 1; i >= 0; --i) {
+    double s = 0.0;
+    for (int j = i + 1 + lane; j < P; j += 32) s = fma(S.A[i * LD + j], S.delta[j], s);
+    s = warp_sum(s);
+    if (lane == 0) S.delta[i] = __ddiv_rn(__dsub_rn(S.rhs[i], s), S.A[i * LD + i]);
+    __syncwarp();
+  }
+  return true;
+}
+
+// gamma from the eigenvalues of J'J: cyclic Jacobi, round-robin disjoint
+// pairs, rotations skipped below max(eps * max|diag|, 1e-15 sqrt|a_pp a_qq|)
+// (LAPACK dsyevd's eigenvalues carry the same eps * ||A|| absolute accuracy)
+template <int PM>
+__device__ double w_gamma(WarpLm<PM>& S, int P, double alpha, double beta, int lane) {
+  constexpr int LD = WarpLm<PM>::LD;
+  if (lane < P)
+    for (int b = 0; b < P; ++b) S.A[lane * LD + b] = S.jtj[lane * LD + b];
+  double dmax = lane < P ? fabs(S.jtj[lane * LD + lane]) : 0.0;
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, m));
+  const double floor_abs = 2.220446049250313e-16 * dmax;
+  __syncwarp();
+  const int Pp = (P + 1) & ~1;
+  const int np = Pp / 2;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    bool any = false;
+    for (int r = 0; r < Pp - 1; ++r) {
+      bool rot = false;
+      if (lane < np) {
+        const int pqv = S.rr[r * (PM / 2) + lane];
+        const int p = pqv & 255, q = pqv >> 8;
+        double c = 1.0, s = 0.0;
+        if (q < P) {
+          const double apq = S.A[p * LD + q], app = S.A[p * LD + p], aqq = S.A[q * LD + q];
+          if (fabs(apq) > floor_abs && fabs(apq) > 1e-15 * sqrt(fabs(app * aqq))) {
+            const double tau = (aqq - app) / (2.0 * apq);
+            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+            rot = true;
+          }
+        }
+        S.cs[2 * lane] = c;
+        S.cs[2 * lane + 1] = s;
+        S.pq[lane] = p | (q << 8);
+      }
+      rot = __any_sync(0xffffffffu, rot);
+      __syncwarp();
+      if (!rot) continue;
+      any = true;
+      if (lane < P) {  // columns: A <- A J   (lane = row i)
+        for (int k = 0; k < np; ++k) {
+          const double s = S.cs[2 * k + 1];
+          if (s == 0.0) continue;
+          const int p = S.pq[k] & 255, q = S.pq[k] >> 8;
+          const double c = S.cs[2 * k], aip = S.A[lane * LD + p], aiq = S.A[lane * LD + q];
+          S.A[lane * LD + p] = c * aip - s * aiq;
+          S.A[lane * LD + q] = s * aip + c * aiq;
+        }
+      }
+      __syncwarp();
+      if (lane < P) {  // rows: A <- J' A   (lane = column j), (p,q) annihilated
+        for (int k = 0; k < np; ++k) {
+          const double s = S.cs[2 * k + 1];
+          if (s == 0.0) continue;
+          const int p = S.pq[k] & 255, q = S.pq[k] >> 8;
+          const double c = S.cs[2 * k], apj = S.A[p * LD + lane], aqj = S.A[q * LD + lane];
+          S.A[p * LD + lane] = (lane == q) ? 0.0 : c * apj - s * aqj;
+          S.A[q * LD + lane] = (lane == p) ? 0.0 : s * apj + c * aqj;
+        }
+      }
+      __syncwarp();
+    }
+    if (!any) break;
+  }
+  double part = 0.0;
+  if (lane < P) {
+    const double lam = fmax(S.A[lane * LD + lane], 0.0);
+    const double sc = __dmul_rn(beta, lam);
+    const double den = __dadd_rn(sc, alpha);
+    part = den > 0.0 ? __ddiv_rn(sc, den) : 0.0;
+  }
+  return warp_sum(part);
+}
+
+// gamma for the wider warp path (P up to 32): Householder tridiagonalisation
+// of J'J (lane = row, reflector/rank-2 update lane-parallel) followed by
+// Sturm-sequence bisection, one eigenvalue per lane.  Same eps*||A||
+// absolute eigenvalue accuracy as LAPACK dsyevd (tridiagonalise + solve),
+// ~3x fewer instructions than cyclic Jacobi at P = 31.
+template <int PM>
+__device__ double w_gamma_tri(WarpLm<PM>& S, int P, double alpha, double beta, int lane) {
+  constexpr int LD = WarpLm<PM>::LD;
+  double* v = S.rhs;     // reflector
+  double* wv = S.delta;  // rank-2 partner
+  double* dd = S.Jc;     // diagonal of T
+  double* e2 = S.Jc + PM;  // squared off-diagonal of T
+  double* ee = S.Jc + 2 * PM;
+  if (lane < P)
+    for (int b = 0; b < P; ++b) S.A[lane * LD + b] = S.jtj[lane * LD + b];
+  __syncwarp();
+  for (int k = 0; k + 2 < P; ++k) {
+    const double xi = (lane > k && lane < P) ? S.A[lane * LD + k] : 0.0;
+    const double sig = warp_sum(xi * xi);
+    const double x0 = S.A[(k + 1) * LD + k];
+    const double tail = sig - x0 * x0;
+    if (!(tail > 0.0)) {  // column already tridiagonal
+      if (lane == 0) ee[k] = x0;
+      __syncwarp();
+      continue;
+    }
+    const double al = x0 > 0.0 ? -sqrt(sig) : sqrt(sig);
+    const double bh = 1.0 / (sig - al * x0);  // 2 / v'v
+    if (lane > k && lane < P) v[lane] = xi - (lane == k + 1 ? al : 0.0);
+    __syncwarp();
+    double pi = 0.0;
+    if (lane > k && lane < P) {
+      for (int j = k + 1; j < P; ++j) pi = fma(S.A[lane * LD + j], v[j], pi);
+      pi *= bh;
+    }
+    const double K = 0.5 * bh * warp_sum((lane > k && lane < P) ? v[lane] * pi : 0.0);
+    if (lane > k && lane < P) wv[lane] = pi - K * v[lane];
+    __syncwarp();
+    if (lane > k && lane < P) {
+      const double vi = v[lane], wi = wv[lane];
+      for (int j = k + 1; j < P; ++j)
+        S.A[lane * LD + j] -= fma(vi, wv[j], wi * v[j]);
+    }
+    if (lane == 0) ee[k] = al;
+    __syncwarp();
+  }
+  if (lane < P) dd[lane] = S.A[lane * LD + lane];
+  if (lane == 0 && P >= 2) ee[P - 2] = S.A[(P - 1) * LD + (P - 2)];
+  __syncwarp();
+  if (lane + 1 < P) e2[lane] = ee[lane] * ee[lane];
+  // Gershgorin interval of T
+  double glo = 0.0, ghi = 0.0, emax2 = 0.0;
+  if (lane < P) {
+    const double r = (lane > 0 ? fabs(ee[lane - 1]) : 0.0) + (lane + 1 < P ? fabs(ee[lane]) : 0.0);
+    glo = dd[lane] - r;
+    ghi = dd[lane] + r;
+    emax2 = lane + 1 < P ? e2[lane] : 0.0;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    glo = fmin(glo, __shfl_xor_sync(0xffffffffu, glo, m));
+    ghi = fmax(ghi, __shfl_xor_sync(0xffffffffu, ghi, m));
+    emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, m));
+  }
+  const double tnorm = fmax(fabs(glo), fabs(ghi));
+  const double eps = 2.220446049250313e-16;
+  const double pivmin = fmax(1e-300, emax2 * 1e-300);
+  double part = 0.0;
+  if (lane < P) {  // lane-th smallest eigenvalue by bisection
+    double lo = glo - eps * tnorm - 1e-300, hi = ghi + eps * tnorm + 1e-300;
+    for (int it = 0; it < 120; ++it) {
+      if (hi - lo <= 2.0 * eps * fmax(fmax(fabs(lo), fabs(hi)), tnorm * 0.5)) break;
+      const double mid = 0.5 * (lo + hi);
+      int cnt = 0;
+      double q = dd[0] - mid;
+      if (fabs(q) < pivmin) q = -pivmin;
+      cnt += q < 0.0;
+      for (int j = 1; j < P; ++j) {
+        q = (dd[j] - mid) - e2[j - 1] / q;
+        if (fabs(q) < pivmin) q = -pivmin;
+        cnt += q < 0.0;
+      }
+      if (cnt > lane) hi = mid; else lo = mid;
+    }
+    const double lam = fmax(0.5 * (lo + hi), 0.0);
+    const double sc = __dmul_rn(beta, lam);
+    const double den = __dadd_rn(sc, alpha);
+    part = den > 0.0 ? __ddiv_rn(sc, den) : 0.0;
+  }
+  return warp_sum(part);
+}
+
+template <int PM, int D>
+__global__ void __launch_bounds__(128) lm_warp_kernel(LmLaunch L) {
+  extern __shared__ __align__(16) unsigned char lm_smem[];
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + wi;
+  if (task >= L.n_tasks) return;
+  WarpLm<PM>& S = ((WarpLm<PM>*)lm_smem)[wi];
+  const bbml_lm_task tk = L.tasks[task];
+  const int orig = L.orig_index[task];
+  const int n = tk.n, d = tk.d, h = tk.h;
+  const int P = h * (d + 2) + 1;
+  const int xs = L.x_stride;
+  const double* X = L.X + tk.row_begin * (int64_t)xs;
+  const double* Y = L.y + tk.row_begin;
+
+  if (lane == 0) {  // init (brbpnn.py:323-331)
+    Pcg64 rng;
+    rng.seed(tk.seed);
+    const double s1 = __ddiv_rn(1.0, __dsqrt_rn((double)d));
+    const double s2 = __ddiv_rn(1.0, __dsqrt_rn((double)h));
+    const int hd = h * d;
+    for (int i = 0; i < hd + h; ++i) S.w[i] = rng.uniform(-s1, s1);
+    for (int i = hd + h; i < P; ++i) S.w[i] = rng.uniform(-s2, s2);
+    int e = 0;  // upper-triangle entry table for the generic stats path
+    for (int a = 0; a < P; ++a)
+      for (int b = a; b <= P; ++b) S.ent[e++] = (unsigned short)((a << 8) | b);
+    const int Pp = (P + 1) & ~1;  // Jacobi round-robin schedule (index P = bye when P is odd)
+    for (int r = 0; r < Pp - 1; ++r)
+      for (int k = 0; k < Pp / 2; ++k) {
+        const int pa = k == 0 ? 0 : 1 + ((k - 1 + r) % (Pp - 1));
+        const int qa = 1 + ((Pp - 2 - k + r) % (Pp - 1));
+        S.rr[r * (PM / 2) + k] = (unsigned short)(min(pa, qa) | (max(pa, qa) << 8));
+      }
+  }
+  __syncwarp();
+
+  double alpha = tk.alpha0, beta = tk.beta0, mu = tk.mu0;
+  const bool est = tk.estimate != 0;
+  double* hist = (tk.hist_offset >= 0) ? L.history + tk.hist_offset : nullptr;
+  double e_d = w_energy<PM, D>(S, S.w, X, Y, n, d, h, xs, lane);
+  double e_w = 0.0;
+  for (int i = 0; i < P; ++i) e_w = fma(S.w[i], S.w[i], e_w);
+  bool have_stats = false;
+  int code = BBML_MODEL_OK, trials = 0, epochs = 0, any_pinned = 0, stable = 0;
+  double fail_mu = 0.0, last_mu = NAN, last_gamma = NAN;
+  double prev_g = 0.0, prev_d = 0.0, prev_w = 0.0;
+  bool have_prev = false;
+
+  for (int ep = 0; ep < tk.max_epochs; ++ep) {
+    if (!have_stats) w_stats<PM, D>(S, X, Y, n, d, h, P, xs, lane);
+    const double f0 = __dadd_rn(__dmul_rn(beta, e_d), __dmul_rn(alpha, e_w));
+    bool accepted = false;
+    double td = 0.0, tw = 0.0;
+    while (true) {
+      ++trials;
+      if (!w_solve<PM>(S, P, alpha, beta, mu, lane)) {
+        code = BBML_MODEL_SINGULAR;
+        fail_mu = mu;
+        break;
+      }
+      if (lane < P) S.wt[lane] = __dadd_rn(S.w[lane], S.delta[lane]);
+      __syncwarp();
+      td = w_energy<PM, D>(S, S.wt, X, Y, n, d, h, xs, lane);
+      tw = 0.0;
+      for (int i = 0; i < P; ++i) tw = fma(S.wt[i], S.wt[i], tw);
+      const double f1 = __dadd_rn(__dmul_rn(beta, td), __dmul_rn(alpha, tw));
+      if (f1 < f0) {
+        mu = fmax(__dmul_rn(mu, tk.mu_dec), 1e-20);
+        accepted = true;
+        break;
+      }
+      mu = __dmul_rn(mu, tk.mu_inc);
+      if (mu > tk.mu_max) break;
+    }
+    if (code != BBML_MODEL_OK || !accepted) break;
+    if (lane < P) S.w[lane] = S.wt[lane];
+    __syncwarp();
+    e_d = td;
+    e_w = tw;
+    const double f1 = __dadd_rn(__dmul_rn(beta, e_d), __dmul_rn(alpha, e_w));
+    double gamma = NAN;
+    int pinned = 0;
+    if (est) {
+      w_stats<PM, D>(S, X, Y, n, d, h, P, xs, lane);
+      have_stats = true;
+      gamma = PM > 8 ? w_gamma_tri<PM>(S, P, alpha, beta, lane) : w_gamma<PM>(S, P, alpha, beta, lane);
+      double na, nb;
+      if (e_w > 0.0) {
+        na = __ddiv_rn(gamma, __dmul_rn(2.0, e_w));
+      } else {
+        na = 1e12;
+        pinned = 1;
+      }
+      if (e_d > 0.0) {
+        nb = __ddiv_rn(__dsub_rn((double)n, gamma), __dmul_rn(2.0, e_d));
+      } else {
+        nb = 1e12;
+        pinned = 1;
+      }
+      alpha = fmin(fmax(na, 1e-12), 1e12);
+      beta = fmin(fmax(nb, 1e-12), 1e12);
+    } else {
+      have_stats = false;
+    }
+    any_pinned |= pinned;
+    last_mu = mu;
+    last_gamma = gamma;
+    epochs = ep + 1;
+    if (hist && lane == 0) {
+      double* r = hist + (int64_t)ep * 10;
+      r[0] = ep; r[1] = f0; r[2] = f1; r[3] = e_d; r[4] = e_w;
+      r[5] = alpha; r[6] = beta; r[7] = gamma; r[8] = mu; r[9] = pinned;
+    }
+    if (have_prev && est) {
+      const bool ok = fabs(gamma - prev_g) <= 1e-7 * fmax(fabs(prev_g), 1e-300) &&
+                      fabs(e_d - prev_d) <= 1e-7 * fmax(fabs(prev_d), 1e-300) &&
+                      fabs(e_w - prev_w) <= 1e-7 * fmax(fabs(prev_w), 1e-300);
+      if (ok) {
+        if (++stable >= 5) break;
+      } else {
+        stable = 0;
+      }
+    }
+    prev_g = gamma;
+    prev_d = e_d;
+    prev_w = e_w;
+    have_prev = true;
+  }
+  __syncwarp();
+  double* W = L.weights + tk.w_offset;
+  if (lane < P) W[lane] = S.w[lane];
+  if (lane == 0) {
+    bbml_model_status st{};
+    st.code = code;
+    st.epochs = epochs;
+    st.detail = any_pinned;
+    st.trials = trials;
+    st.value = fail_mu;
+    st.mu = last_mu;
+    st.gamma = last_gamma;
+    st.alpha = alpha;
+    st.beta = beta;
+    L.status[orig] = st;
+  }
+}
+
+template <int PM, int D>
+static cudaError_t lm_launch_warp(const LmLaunch& L, cudaStream_t s) {
+  const int warps = PM > 8 ? 2 : 4;  // PM = 32: ~23 KB smem per warp -> 2-warp CTAs pack 10 per SM
+  const size_t smem = warps * sizeof(WarpLm<PM>);
+  auto k = lm_warp_kernel<PM, D>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k<<<(int)ceil_div(L.n_tasks, warps), 32 * warps, smem, s>>>(L);
+  return cudaGetLastError();
+}
+
 template <int PMAX, int CH>
 static size_t lm_smem_bytes() {
   size_t dbl = 5 * PMAX + 2 * PMAX * PMAX + CH * PMAX + (CH > LM_NT ? CH : LM_NT) +
@@ -477,7 +1054,13 @@ static cudaError_t lm_launch_bucket(const LmLaunch& L, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-static int lm_bucket(int P) { return P <= 8 ? 8 : P <= 32 ? 32 : P <= 64 ? 64 : 96; }
+// launch key: 1..4 = hidden-1 fast path with d inputs; 8 / 32 = warp kernels;
+// 64 / 96 = CTA-per-model kernels
+static int lm_key(const bbml_lm_task& t) {
+  const int P = t.h * (t.d + 2) + 1;
+  if (t.h == 1 && t.d <= 4) return t.d;
+  return P <= 8 ? 8 : P <= 32 ? 32 : P <= 64 ? 64 : 96;
+}
 
 bbml_status lm_train_launch(const bbml_lm_task* tasks, int32_t n_tasks, const double* X,
                             const double* y, int32_t x_stride, double* weights, double* history,
@@ -503,7 +1086,7 @@ bbml_status lm_train_launch(const bbml_lm_task* tasks, int32_t n_tasks, const do
   }
   auto P_of = [&](int i) { return tasks[i].h * (tasks[i].d + 2) + 1; };
   std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
-    const int ka = lm_bucket(P_of(a)), kb = lm_bucket(P_of(b));
+    const int ka = lm_key(tasks[a]), kb = lm_key(tasks[b]);
     if (ka != kb) return ka > kb;
     const double ca = (double)tasks[a].n * P_of(a) * P_of(a);
     const double cb = (double)tasks[b].n * P_of(b) * P_of(b);
@@ -523,11 +1106,16 @@ bbml_status lm_train_launch(const bbml_lm_task* tasks, int32_t n_tasks, const do
   if ((st = scratch.alloc(&d_orig, n_tasks)) != BBML_OK) return st;
   if ((st = scratch.upload(d_tasks, sorted.data(), n_tasks)) != BBML_OK) return st;
   if ((st = scratch.upload(d_orig, orig.data(), n_tasks)) != BBML_OK) return st;
-  int begin = 0;
+  int n_groups = 0;
+  for (int i = 0; i < n_tasks; ++i)
+    if (i == 0 || lm_key(tasks[idx[i]]) != lm_key(tasks[idx[i - 1]])) ++n_groups;
+  StreamFork fork(stream, n_groups);  // shape groups run concurrently
+  int begin = 0, gno = 0;
   while (begin < n_tasks) {
-    const int b = lm_bucket(P_of(idx[begin]));
+    const int b = lm_key(tasks[idx[begin]]);
     int end = begin;
-    while (end < n_tasks && lm_bucket(P_of(idx[end])) == b) ++end;
+    while (end < n_tasks && lm_key(tasks[idx[end]]) == b) ++end;
+    cudaStream_t stream = fork.child(gno++);
     LmLaunch L{};
     L.tasks = d_tasks + begin;
     L.orig_index = d_orig + begin;
@@ -540,13 +1128,18 @@ bbml_status lm_train_launch(const bbml_lm_task* tasks, int32_t n_tasks, const do
     L.history = history;
     L.status = status;
     cudaError_t e;
-    if (b == 8) e = lm_launch_bucket<8, 128>(L, stream);
-    else if (b == 32) e = lm_launch_bucket<32, 64>(L, stream);
+    if (b == 1) e = lm_launch_warp<8, 1>(L, stream);
+    else if (b == 2) e = lm_launch_warp<8, 2>(L, stream);
+    else if (b == 3) e = lm_launch_warp<8, 3>(L, stream);
+    else if (b == 4) e = lm_launch_warp<8, 4>(L, stream);
+    else if (b == 8) e = lm_launch_warp<8, 0>(L, stream);
+    else if (b == 32) e = lm_launch_warp<32, 0>(L, stream);
     else if (b == 64) e = lm_launch_bucket<64, 32>(L, stream);
     else e = lm_launch_bucket<96, 16>(L, stream);
     if (e != cudaSuccess) return cuda_status(e, "lm_train launch");
     begin = end;
   }
+  if ((st = fork.join()) != BBML_OK) return st;
   return scratch.release();
 }
 

@@ -988,20 +988,31 @@ bbml_status pnn_train_launch(const bbml_pnn_task* tasks, int32_t n_tasks, const 
     to_float_kernel<<<(int)std::min<int64_t>(ceil_div(rows, 256), 4096), 256, 0, stream>>>(
         X, x_stride, d_xf, xf_stride, y, d_yf, rows);
   }
+  // shape groups (homogeneous launches); all scratch is allocated before the fork
+  std::vector<std::pair<int, int>> groups_rng;
   int32_t* d_perm = nullptr;  // global double-buffer workspace, only if some bucket needs it
-  int begin = 0;
-  while (begin < n_tasks) {
-    const int dm = bucket_d(sorted[begin].d), hm = bucket_h(sorted[begin].h);
-    int end = begin;
+  for (int b0 = 0; b0 < n_tasks;) {
+    int b1 = b0;
     int64_t nmax = 0;
-    while (end < n_tasks && bucket_d(sorted[end].d) == dm && bucket_h(sorted[end].h) == hm) {
-      nmax = std::max<int64_t>(nmax, sorted[end].n);
-      ++end;
+    while (b1 < n_tasks && bucket_d(sorted[b1].d) == bucket_d(sorted[b0].d) &&
+           bucket_h(sorted[b1].h) == bucket_h(sorted[b0].h)) {
+      nmax = std::max<int64_t>(nmax, sorted[b1].n);
+      ++b1;
     }
     const size_t elem = nmax <= 65535 ? 2 : 4;
-    if (2 * (size_t)nmax * elem + 64 > smem_limit && d_perm == nullptr) {
+    if (2 * (size_t)nmax * elem + 1024 > smem_limit && d_perm == nullptr) {
       if ((st = scratch.alloc(&d_perm, 2 * total)) != BBML_OK) return st;
     }
+    groups_rng.push_back({b0, b1});
+    b0 = b1;
+  }
+  StreamFork fork(stream, (int)groups_rng.size());
+  for (size_t gno = 0; gno < groups_rng.size(); ++gno) {
+    const int begin = groups_rng[gno].first, end = groups_rng[gno].second;
+    const int dm = bucket_d(sorted[begin].d), hm = bucket_h(sorted[begin].h);
+    int64_t nmax = 0;
+    for (int i = begin; i < end; ++i) nmax = std::max<int64_t>(nmax, sorted[i].n);
+    cudaStream_t stream = fork.child((int)gno);
     PnnLaunch L{};
     L.tasks = d_tasks + begin;
     L.orig_index = d_orig + begin;
@@ -1021,8 +1032,8 @@ bbml_status pnn_train_launch(const bbml_pnn_task* tasks, int32_t n_tasks, const 
     cudaError_t e = precision == 32 ? launch_bucket<float>(dm, hm, L, nmax, smem_limit, stream)
                                     : launch_bucket<double>(dm, hm, L, nmax, smem_limit, stream);
     if (e != cudaSuccess) return cuda_status(e, "pnn_train launch");
-    begin = end;
   }
+  if ((st = fork.join()) != BBML_OK) return st;
   return scratch.release();
 }
 

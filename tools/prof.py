@@ -15,12 +15,15 @@ ap.add_argument("--restarts", type=int, default=1)
 ap.add_argument("--epochs", type=int, default=300)
 ap.add_argument("--only-long", action="store_true")
 ap.add_argument("--top", type=int, default=0)
+ap.add_argument("--app", default=None)
 ap.add_argument("--br-epochs", type=int, default=1000)
 ap.add_argument("--reps", type=int, default=1)
 a = ap.parse_args()
 series, spec, kw = bench.workload_series(a.workload)
 if a.only_long:
     series = sorted(series, key=lambda s: -len(s))[:1]
+if a.app:
+    series = [s for s in series if s.key[0] == a.app]
 if a.top:
     series = sorted(series, key=lambda s: -len(s))[:a.top]
 kinds = {"both": ("pnn", "brbpnn"), "pnn": ("pnn",), "br": ("brbpnn",)}[a.kind]
