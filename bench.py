@@ -47,7 +47,7 @@ def parse():
     return ap.parse_args()
 
 
-DEFAULT_RESTARTS = {"suite16": 8, "app20": 1, "sweep": 16, "wide": 1}
+DEFAULT_RESTARTS = {"suite16": 32, "app20": 1, "sweep": 16, "wide": 1}
 
 
 def workload_series(name: str):
@@ -79,6 +79,16 @@ def pnn_flops(n, d, h, epochs, batch):
     P = h * (d + 2) + 1
     steps = -(-n // batch)
     return epochs * (n * (4 * h * d + 10 * h + 14) + steps * 13 * P)
+
+
+def lm_flops(n, d, h, epochs, trials):
+    """SURVEY §8d algorithmic FLOPs of one BR-BPNN model given its epochs and
+    LM trials: per epoch one J/J'J/J'r pass + the tridiagonal eigen-solve,
+    per trial one damped solve + trial objective."""
+    P = h * (d + 2) + 1
+    per_epoch = n * (P * (P + 1) + 2 * P + 3 * h * d + 10 * h + 1) + 4 * P ** 3 / 3
+    per_trial = P ** 3 / 3 + 2 * P ** 2 + n * (2 * h * d + 7 * h + 4)
+    return epochs * per_epoch + trials * per_trial
 
 
 def sample_clocks(stop_path):
@@ -189,7 +199,7 @@ def reference_arm(args, world, rank):
     series, spec, kw = workload_series(args.workload)
     restarts = args.restarts or DEFAULT_RESTARTS[args.workload]
     cores = os.cpu_count() or 1
-    sample = args.cpu_sample or max(8, cores)
+    sample = args.cpu_sample or max(32, 4 * cores)
     vals = []
     for i in range(args.warmup + args.steps):
         r = run_cpu(series, spec, kw, restarts, sample, cores)
@@ -286,23 +296,35 @@ def main():
         clk.wait()
 
     # dominant kernel (PNN train) timed alone on its stream for the roofline
-    pnn_ms = None
-    if len(wl.pnn):
-        from paper_2202_07798_b200._lib import check, lib, ptr
+    # each training kernel timed alone on its launching stream (CUDA events)
+    from paper_2202_07798_b200._lib import check, lib, ptr
 
+    def timed(fn):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = []
         for _ in range(2):
             flush.fill_(1.0)
             e0.record(s)
-            check(lib().bbml_pnn_train(ptr(dev.pnn_tab), len(dev.pnn_tab), ptr(dev.X), ptr(dev.y),
-                                       wl.train.stride, ptr(dev.weights), None, ptr(dev.status),
-                                       wl.precision, s.cuda_stream), "pnn")
+            fn()
             e1.record(s)
             e1.synchronize()
             reps.append(e0.elapsed_time(e1))
-        pnn_ms = float(np.mean(reps))
-    peak = measure_fma_peak(torch, args.precision)
+        return float(np.mean(reps))
+
+    pnn_ms = lm_ms = None
+    if len(wl.pnn):
+        pnn_ms = timed(lambda: check(lib().bbml_pnn_train(
+            ptr(dev.pnn_tab), len(dev.pnn_tab), ptr(dev.X), ptr(dev.y), wl.train.stride,
+            ptr(dev.weights), None, ptr(dev.status), wl.precision, s.cuda_stream), "pnn"))
+    if len(wl.lm):
+        off = 8 * int(wl.P_pnn.sum())
+        lm_ms = timed(lambda: check(lib().bbml_lm_train(
+            ptr(dev.lm_tab), len(dev.lm_tab), ptr(dev.X), ptr(dev.y), wl.train.stride,
+            ptr(dev.weights) + off, None, ptr(dev.status) + STATUS.itemsize * len(wl.pnn),
+            s.cuda_stream), "lm"))
+    st_all = dev.fetch()["status"]
+    peak32 = measure_fma_peak(torch, 32)
+    peak64 = measure_fma_peak(torch, 64)
 
     t = torch.tensor([total_s, max(e2e_times)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -313,13 +335,32 @@ def main():
     e2e_value = models_per_step / e2e_max
 
     if rank == 0:
-        flops = sum(pnn_flops(int(r["n"]), int(r["d"]), int(r["h"]), int(r["epochs"]), int(r["batch"]))
-                    for r in wl.pnn)
-        achieved = flops / (pnn_ms * 1e-3) / 1e12 if pnn_ms else None
+        peak_p = peak32 if args.precision == 32 else peak64
+        pnn_fl = sum(pnn_flops(int(r["n"]), int(r["d"]), int(r["h"]), int(r["epochs"]), int(r["batch"]))
+                     for r in wl.pnn)
+        st_lm = st_all[len(wl.pnn):]
+        lm_fl = sum(lm_flops(int(r["n"]), int(r["d"]), int(r["h"]), int(e), int(t))
+                    for r, e, t in zip(wl.lm, st_lm["epochs"], st_lm["trials"]))
+        rl = {}
+        if pnn_ms:
+            a = pnn_fl / (pnn_ms * 1e-3) / 1e12
+            rl["pnn"] = {"bound": f"fp{args.precision}-pipe", "kernel": "pnn_lat_kernel (bbml_pnn_train)",
+                         "achieved": a, "peak": peak_p, "unit": "TFLOP/s", "frac": a / peak_p,
+                         "kernel_ms": pnn_ms, "algorithmic_flops": pnn_fl, "traffic": None}
+        if lm_ms:
+            a = lm_fl / (lm_ms * 1e-3) / 1e12
+            rl["lm"] = {"bound": "fp64-pipe", "kernel": "lm_warp_kernel (bbml_lm_train)",
+                        "achieved": a, "peak": peak64, "unit": "TFLOP/s", "frac": a / peak64,
+                        "kernel_ms": lm_ms, "algorithmic_flops": lm_fl, "traffic": None}
+        dom = max(rl, key=lambda k: rl[k]["kernel_ms"]) if rl else None
+        roof = dict(rl[dom]) if dom else {}
+        roof["peak_source"] = ("measured: bbml_fma_peak FMA-pipe microbenchmark on this GPU "
+                               "(MEASURED_PEAKS.json has only HBM / bf16-GEMM peaks)")
+        roof["other"] = {k: v for k, v in rl.items() if k != dom}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
-            r = run_cpu(series, spec, kw, restarts, args.cpu_sample or max(8, cores), cores)
+            r = run_cpu(series, spec, kw, restarts, args.cpu_sample or max(32, 4 * cores), cores)
             cpu = {"value": r["models_per_s"], "unit": "models/s", "cores": cores, "kind": "port",
                    "sample": f"{r['n']} stratified tasks (median pick per equal-count cost stratum) "
                              f"of {args.workload}; ideal-pool throughput = cores / mean per-model "
@@ -337,11 +378,7 @@ def main():
                        "split": spec.mode.value},
             "e2e": {"value": e2e_value, "unit": "models/s", "h2d_bytes_per_step": dev.h2d_bytes,
                     "d2h_bytes_per_step": dev.d2h_bytes},
-            "roofline": {"bound": f"fp{args.precision}-pipe", "kernel": "pnn_train_kernel",
-                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": (achieved / peak) if achieved and peak else None,
-                         "peak_source": "bbml_fma_peak microbenchmark on this GPU (FMA pipe)",
-                         "kernel_ms": pnn_ms, "algorithmic_flops": flops, "traffic": None},
+            "roofline": roof,
             "gpu_launches": launches,
             "models_failed": n_bad,
             "clocks": summarize_clocks(clock_path, local),

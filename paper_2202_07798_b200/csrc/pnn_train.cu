@@ -568,8 +568,12 @@ __global__ void pnn_train_kernel(PnnLaunch L) {
 //   backward   : per-unit gradient sums over the lane's SP samples, then one
 //                xor-16 shuffle joins the halves at the end of the minibatch
 // ------------------------------------------------------------------------
+// NPW producer warps per CTA of 4 models: 4 (one per model) for long series,
+// 1 shared producer for short ones (then 2 CTAs fit per SM: <= 204 registers).
+// The long-series variant is left unconstrained: ptxas' larger allocation
+// (~240 registers) measured ~25% lower per-step latency on the critical path.
 template <typename T, int DM, int SP, typename PermT>
-__global__ void pnn_lat_kernel(PnnLaunch L) {
+__device__ __forceinline__ void pnn_lat_body(const PnnLaunch& L) {
   using A = Arith<T>;
   const int groups = L.groups_per_cta;  // one model per consumer warp
   const int cons_threads = groups * 32;
@@ -839,6 +843,17 @@ __global__ void pnn_lat_kernel(PnnLaunch L) {
   }
 }
 
+// long series: 4 consumer + 4 producer warps, register allocation unconstrained
+template <typename T, int DM, int SP, typename PermT>
+__global__ void pnn_lat_kernel(PnnLaunch L) {
+  pnn_lat_body<T, DM, SP, PermT>(L);
+}
+// short series: 4 consumer + 1 shared producer warp, 2 CTAs per SM
+template <typename T, int DM, int SP, typename PermT>
+__global__ void __launch_bounds__(160, 2) pnn_lat_kernel_shared(PnnLaunch L) {
+  pnn_lat_body<T, DM, SP, PermT>(L);
+}
+
 // ------------------------------------------------------------------------
 // host dispatch
 // ------------------------------------------------------------------------
@@ -859,34 +874,56 @@ __global__ void to_float_kernel(const double* __restrict__ X, int xs, float* __r
 
 static int bucket_d(int d) { return d <= 2 ? 2 : d <= 4 ? 4 : 16; }
 static int bucket_h(int h) { return h <= 16 ? 16 : 64; }
+// series at least this long get a dedicated producer warp (see launch_variant)
+constexpr int kLongSeries = 2048;
+// BBML_PNN_SPLIT=1 launches short series separately with a shared producer
+// warp (more CTAs per SM).  Off by default: measured slower on suite16
+// because the co-resident short-series warps stretch the critical chains.
+static bool split_long_short() {
+  static const bool on = [] {
+    const char* e = getenv("BBML_PNN_SPLIT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+static int bucket_n(int n) { return (split_long_short() && n < kLongSeries) ? 0 : 1; }
 
 template <typename T, int DM, int HM, typename PermT>
 static cudaError_t launch_variant(PnnLaunch L, int64_t nmax, size_t smem_limit, cudaStream_t s) {
   constexpr bool LAT = HM <= 16;  // h <= 16: warp-per-model latency kernel
   constexpr int G = 32;
   constexpr int SC = 10;
-  // models per CTA; each model gets its own warp-cooperative producer warp
-  // (one sequential Fisher-Yates scan keeps up with one consumer warp)
+  // 4 models per CTA.  Long series: one warp-cooperative producer warp per
+  // model (one sequential Fisher-Yates scan keeps up with one consumer warp).
+  // Short series (n < kLongSeries): one producer serves the 4 models, so the
+  // CTA is 5 warps and two CTAs fit per SM.
+  const bool shared_prod = LAT && nmax < kLongSeries;
   const int groups_max = 4;
-  const size_t flags = pnn_smem_header(groups_max, groups_max);
+  const int npw_max = shared_prod ? 1 : groups_max;
+  const size_t flags = pnn_smem_header(groups_max, npw_max);
   const size_t per_group = 2 * (size_t)nmax * sizeof(PermT);
   int groups = (int)std::min<size_t>(groups_max, (smem_limit - flags) / per_group);
   size_t smem;
+  int npw;
   if (groups >= 1) {
+    npw = shared_prod ? 1 : groups;
     L.perm_in_smem = 1;
     L.perm_cap = (int32_t)nmax;
-    smem = pnn_smem_header(groups, groups) + (size_t)groups * per_group;
+    smem = pnn_smem_header(groups, npw) + (size_t)groups * per_group;
   } else {
     groups = groups_max;
+    npw = groups;
     L.perm_in_smem = 0;
     L.perm_cap = 0;
-    smem = pnn_smem_header(groups, groups);
+    smem = pnn_smem_header(groups, npw);
   }
   L.groups_per_cta = groups;
   const int cons = ((groups * G + 31) / 32) * 32;
-  const int prod = 32 * groups;
+  const int prod = 32 * npw;
   const int blocks = (int)ceil_div(L.n_tasks, groups);
-  auto k = LAT ? pnn_lat_kernel<T, DM, 5, PermT> : pnn_train_kernel<T, DM, HM, G, SC, PermT>;
+  auto k = !LAT ? pnn_train_kernel<T, DM, HM, G, SC, PermT>
+                : (npw == 1 && shared_prod ? pnn_lat_kernel_shared<T, DM, 5, PermT>
+                                           : pnn_lat_kernel<T, DM, 5, PermT>);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -943,8 +980,8 @@ bbml_status pnn_train_launch(const bbml_pnn_task* tasks, int32_t n_tasks, const 
   };
   // homogeneous launches per (d, h) bucket; longest sequential chains first
   std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
-    const int ka = bucket_d(tasks[a].d) * 1000 + bucket_h(tasks[a].h);
-    const int kb = bucket_d(tasks[b].d) * 1000 + bucket_h(tasks[b].h);
+    const int ka = bucket_d(tasks[a].d) * 1000 + bucket_h(tasks[a].h) * 2 + bucket_n(tasks[a].n);
+    const int kb = bucket_d(tasks[b].d) * 1000 + bucket_h(tasks[b].h) * 2 + bucket_n(tasks[b].n);
     if (ka != kb) return ka < kb;
     return cost(a) > cost(b);
   });
@@ -995,7 +1032,8 @@ bbml_status pnn_train_launch(const bbml_pnn_task* tasks, int32_t n_tasks, const 
     int b1 = b0;
     int64_t nmax = 0;
     while (b1 < n_tasks && bucket_d(sorted[b1].d) == bucket_d(sorted[b0].d) &&
-           bucket_h(sorted[b1].h) == bucket_h(sorted[b0].h)) {
+           bucket_h(sorted[b1].h) == bucket_h(sorted[b0].h) &&
+           bucket_n(sorted[b1].n) == bucket_n(sorted[b0].n)) {
       nmax = std::max<int64_t>(nmax, sorted[b1].n);
       ++b1;
     }
