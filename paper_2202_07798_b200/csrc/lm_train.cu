@@ -855,7 +855,16 @@ __device__ double w_gamma_tri(WarpLm<PM>& S, int P, double alpha, double beta, i
   if (lane < P) {  // lane-th smallest eigenvalue by bisection
     double lo = glo - eps * tnorm - 1e-300, hi = ghi + eps * tnorm + 1e-300;
     for (int it = 0; it < 120; ++it) {
-      if (hi - lo <= 2.0 * eps * fmax(fmax(fabs(lo), fabs(hi)), tnorm * 0.5)) break;
+      // stop once the eigenvalue's gamma contribution beta*l/(beta*l+alpha) is
+      // pinned to 1e-13 (near-null eigenvalues, which decide gamma when alpha
+      // is tiny, are resolved far below alpha/beta), at relative precision, or
+      // when the interval is entirely <= 0 (clipped to 0)
+      if (hi <= 0.0 || hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 1e-290) break;
+      {
+        const double chi = beta * hi / (beta * hi + alpha);
+        const double clo = lo > 0.0 ? beta * lo / (beta * lo + alpha) : 0.0;
+        if (chi - clo <= 1e-13) break;
+      }
       const double mid = 0.5 * (lo + hi);
       int cnt = 0;
       double q = dd[0] - mid;
@@ -1035,32 +1044,19 @@ static cudaError_t lm_launch_warp(const LmLaunch& L, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int PMAX, int CH>
-static size_t lm_smem_bytes() {
-  size_t dbl = 5 * PMAX + 2 * PMAX * PMAX + CH * PMAX + (CH > LM_NT ? CH : LM_NT) +
-               2 * (PMAX + 2) + LM_WARPS + 2 + (PMAX + 1) / 2 + 1 + 4;
-  return dbl * sizeof(double);
-}
-
-template <int PMAX, int CH>
-static cudaError_t lm_launch_bucket(const LmLaunch& L, cudaStream_t s) {
-  const size_t smem = lm_smem_bytes<PMAX, CH>();
-  auto k = lm_train_kernel<PMAX, CH>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  k<<<L.n_tasks, LM_NT, smem, s>>>(L);
-  return cudaGetLastError();
-}
-
-// launch key: 1..4 = hidden-1 fast path with d inputs; 8 / 32 = warp kernels;
-// 64 / 96 = CTA-per-model kernels
+// launch key: 1..4 = hidden-1 warp fast path with d inputs; 8 / 32 = warp
+// kernels (P <= 8 / P <= 32); 512 = wide CTA-per-model kernel (lm_wide.cu)
 static int lm_key(const bbml_lm_task& t) {
   const int P = t.h * (t.d + 2) + 1;
   if (t.h == 1 && t.d <= 4) return t.d;
-  return P <= 8 ? 8 : P <= 32 ? 32 : P <= 64 ? 64 : 96;
+  return P <= 8 ? 8 : P <= 32 ? 32 : 512;
 }
+
+bbml_status lm_wide_launch(const bbml_lm_task* d_tasks, const int32_t* d_orig,
+                           const bbml_lm_task* h_tasks, int32_t n_tasks, const double* X,
+                           const double* y, int32_t x_stride, double* weights, double* history,
+                           bbml_model_status* status, ScratchBuffer& scratch, cudaStream_t s,
+                           bool alloc_only, double** slabs);
 
 bbml_status lm_train_launch(const bbml_lm_task* tasks, int32_t n_tasks, const double* X,
                             const double* y, int32_t x_stride, double* weights, double* history,
@@ -1074,7 +1070,7 @@ bbml_status lm_train_launch(const bbml_lm_task* tasks, int32_t n_tasks, const do
       return BBML_ERR_INVALID;
     }
     const int P = t.h * (t.d + 2) + 1;
-    if (t.d > BBML_MAX_INPUTS || P > 96) {
+    if (t.d > BBML_MAX_INPUTS || P > BBML_LM_MAX_PARAMS) {
       set_error("lm task %d: d=%d h=%d (P=%d) outside the supported envelope", i, t.d, t.h, P);
       return BBML_ERR_UNSUPPORTED;
     }
@@ -1106,16 +1102,33 @@ bbml_status lm_train_launch(const bbml_lm_task* tasks, int32_t n_tasks, const do
   if ((st = scratch.alloc(&d_orig, n_tasks)) != BBML_OK) return st;
   if ((st = scratch.upload(d_tasks, sorted.data(), n_tasks)) != BBML_OK) return st;
   if ((st = scratch.upload(d_orig, orig.data(), n_tasks)) != BBML_OK) return st;
-  int n_groups = 0;
-  for (int i = 0; i < n_tasks; ++i)
-    if (i == 0 || lm_key(tasks[idx[i]]) != lm_key(tasks[idx[i - 1]])) ++n_groups;
-  StreamFork fork(stream, n_groups);  // shape groups run concurrently
-  int begin = 0, gno = 0;
-  while (begin < n_tasks) {
-    const int b = lm_key(tasks[idx[begin]]);
-    int end = begin;
-    while (end < n_tasks && lm_key(tasks[idx[end]]) == b) ++end;
-    cudaStream_t stream = fork.child(gno++);
+  std::vector<std::pair<int, int>> groups;
+  for (int b0 = 0; b0 < n_tasks;) {
+    int b1 = b0;
+    while (b1 < n_tasks && lm_key(sorted[b1]) == lm_key(sorted[b0])) ++b1;
+    groups.push_back({b0, b1});
+    b0 = b1;
+  }
+  // wide slabs are allocated on the parent stream before the fork
+  double* wide_slabs = nullptr;
+  for (auto& g : groups)
+    if (lm_key(sorted[g.first]) == 512)
+      if ((st = lm_wide_launch(nullptr, nullptr, sorted.data() + g.first, g.second - g.first, X, y,
+                               x_stride, weights, history, status, scratch, stream, true,
+                               &wide_slabs)) != BBML_OK)
+        return st;
+  StreamFork fork(stream, (int)groups.size());  // shape groups run concurrently
+  for (size_t gno = 0; gno < groups.size(); ++gno) {
+    const int begin = groups[gno].first, end = groups[gno].second;
+    const int b = lm_key(sorted[begin]);
+    cudaStream_t cs = fork.child((int)gno);
+    if (b == 512) {
+      if ((st = lm_wide_launch(d_tasks + begin, d_orig + begin, sorted.data() + begin, end - begin, X,
+                               y, x_stride, weights, history, status, scratch, cs, false,
+                               &wide_slabs)) != BBML_OK)
+        return st;
+      continue;
+    }
     LmLaunch L{};
     L.tasks = d_tasks + begin;
     L.orig_index = d_orig + begin;
@@ -1128,16 +1141,13 @@ bbml_status lm_train_launch(const bbml_lm_task* tasks, int32_t n_tasks, const do
     L.history = history;
     L.status = status;
     cudaError_t e;
-    if (b == 1) e = lm_launch_warp<8, 1>(L, stream);
-    else if (b == 2) e = lm_launch_warp<8, 2>(L, stream);
-    else if (b == 3) e = lm_launch_warp<8, 3>(L, stream);
-    else if (b == 4) e = lm_launch_warp<8, 4>(L, stream);
-    else if (b == 8) e = lm_launch_warp<8, 0>(L, stream);
-    else if (b == 32) e = lm_launch_warp<32, 0>(L, stream);
-    else if (b == 64) e = lm_launch_bucket<64, 32>(L, stream);
-    else e = lm_launch_bucket<96, 16>(L, stream);
+    if (b == 1) e = lm_launch_warp<8, 1>(L, cs);
+    else if (b == 2) e = lm_launch_warp<8, 2>(L, cs);
+    else if (b == 3) e = lm_launch_warp<8, 3>(L, cs);
+    else if (b == 4) e = lm_launch_warp<8, 4>(L, cs);
+    else if (b == 8) e = lm_launch_warp<8, 0>(L, cs);
+    else e = lm_launch_warp<32, 0>(L, cs);
     if (e != cudaSuccess) return cuda_status(e, "lm_train launch");
-    begin = end;
   }
   if ((st = fork.join()) != BBML_OK) return st;
   return scratch.release();

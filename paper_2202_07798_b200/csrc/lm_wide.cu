@@ -1,0 +1,553 @@
+// lm_wide.cu — BR-BPNN Levenberg-Marquardt trainer for wide networks
+// (33 <= P <= 512, e.g. hidden 64 at d = 2 -> P = 257; BASELINE config 5).
+//
+// Same semantics as lm_train.cu (brbpnn.py:286-346, see there for line refs),
+// one model per CTA of 256 threads.  The P x P matrices (J'J and the LU /
+// tridiagonalisation workspace) and the n x P Jacobian live in a per-model
+// global scratch slab that stays L2-resident (126 MB L2); vectors live in
+// shared memory.
+//   J'J        : 4x4 register tiles over the upper triangle, streamed over the
+//                n Jacobian rows (J written once per pass by the row kernel)
+//   solve      : right-looking LU with partial pivoting (dgetf2 order), block
+//                argmax, triangular solves with block reductions
+//   gamma      : Householder tridiagonalisation + Sturm bisection (one or two
+//                eigenvalues per thread), like LAPACK dsytrd + dstebz
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "launch.h"
+#include "pcg64.cuh"
+
+namespace bbml {
+
+constexpr int WNT = 256;
+constexpr int WWARPS = WNT / 32;
+constexpr int WPMAX = 512;
+
+struct WideLaunch {
+  const bbml_lm_task* tasks;
+  const int32_t* orig_index;
+  int32_t n_tasks;
+  int32_t x_stride;
+  const double* X;
+  const double* y;
+  double* weights;
+  double* history;
+  bbml_model_status* status;
+  double* scratch;        // per CTA slab
+  int64_t slab_doubles;   // doubles per slab
+  int32_t ld;             // leading dimension of the P x P matrices (>= P, multiple of 4)
+};
+
+struct WideSmem {
+  double w[WPMAX], wt[WPMAX], delta[WPMAX], jtr[WPMAX], rhs[WPMAX];
+  double v[WPMAX], pv[WPMAX], dd[WPMAX], ee[WPMAX], e2[WPMAX];
+  double red[WWARPS * 2];
+  int ired[WWARPS];
+  int piv;
+};
+
+__device__ __forceinline__ double bsum(double x, WideSmem& S) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) x += __shfl_xor_sync(0xffffffffu, x, m);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) S.red[threadIdx.x >> 5] = x;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < WWARPS; ++i) s += S.red[i];
+  return s;
+}
+
+__device__ __forceinline__ double bmax(double x, WideSmem& S) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, m));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) S.red[threadIdx.x >> 5] = x;
+  __syncthreads();
+  double s = S.red[0];
+#pragma unroll
+  for (int i = 1; i < WWARPS; ++i) s = fmax(s, S.red[i]);
+  return s;
+}
+
+// forward of one sample (brbpnn.forward) and optionally its Jacobian row
+__device__ __forceinline__ double wide_sample(const double* __restrict__ w, const double* x, int d,
+                                              int h, double* jrow) {
+  const int hd = h * d;
+  double out = 0.0;
+  for (int j = 0; j < h; ++j) {
+    double pre = 0.0;
+    for (int k = 0; k < d; ++k) pre = fma(x[k], w[j * d + k], pre);
+    const double a = tansig(__dadd_rn(pre, w[hd + j]));
+    const double w2 = w[hd + h + j];
+    out = fma(a, w2, out);
+    if (jrow) {
+      const double da = __dmul_rn(__dsub_rn(1.0, __dmul_rn(a, a)), w2);
+      for (int k = 0; k < d; ++k) jrow[j * d + k] = __dmul_rn(da, x[k]);
+      jrow[hd + j] = da;
+      jrow[hd + h + j] = a;
+    }
+  }
+  if (jrow) jrow[hd + 2 * h] = 1.0;
+  return __dadd_rn(out, w[hd + 2 * h]);
+}
+
+__device__ double wide_energy(const double* wv, const double* X, const double* Y, int n, int d, int h,
+                              int xs, WideSmem& S) {
+  double acc = 0.0, x[BBML_MAX_INPUTS];
+  for (int i = threadIdx.x; i < n; i += WNT) {
+    for (int k = 0; k < d; ++k) x[k] = __ldg(X + (int64_t)i * xs + k);
+    const double r = __dsub_rn(wide_sample(wv, x, d, h, nullptr), __ldg(Y + i));
+    acc = fma(r, r, acc);
+  }
+  return bsum(acc, S);
+}
+
+// J (n x ldj) rows + residuals, then J'J (upper 4x4 tiles, mirrored) and J'r
+__device__ void wide_stats(double* J, double* R, double* jtj, int ld, const double* X, const double* Y,
+                           int n, int d, int h, int P, int xs, WideSmem& S) {
+  double x[BBML_MAX_INPUTS];
+  for (int i = threadIdx.x; i < n; i += WNT) {
+    for (int k = 0; k < d; ++k) x[k] = __ldg(X + (int64_t)i * xs + k);
+    double* jr = J + (int64_t)i * ld;
+    R[i] = __dsub_rn(wide_sample(S.w, x, d, h, jr), __ldg(Y + i));
+    for (int c = P; c < ld; ++c) jr[c] = 0.0;
+  }
+  __syncthreads();
+  const int nt = ld / 4;
+  const int ntiles = nt * (nt + 1) / 2;
+  for (int t = threadIdx.x; t < ntiles; t += WNT) {
+    int ta = 0, rem = t;  // t -> (ta <= tb) row-major upper triangle of tiles
+    while (rem >= nt - ta) {
+      rem -= nt - ta;
+      ++ta;
+    }
+    const int tb = ta + rem;
+    double acc[4][4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[p][q] = 0.0;
+#pragma unroll 4
+    for (int c = 0; c < n; ++c) {
+      const double4 ja = *(const double4*)(J + (int64_t)c * ld + 4 * ta);
+      const double4 jb = *(const double4*)(J + (int64_t)c * ld + 4 * tb);
+      const double va[4] = {ja.x, ja.y, ja.z, ja.w}, vb[4] = {jb.x, jb.y, jb.z, jb.w};
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = fma(va[p], vb[q], acc[p][q]);
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int a = 4 * ta + p, b = 4 * tb + q;
+        jtj[(int64_t)a * ld + b] = acc[p][q];
+        jtj[(int64_t)b * ld + a] = acc[p][q];
+      }
+  }
+  for (int a = threadIdx.x; a < P; a += WNT) {
+    double s = 0.0;
+    for (int c = 0; c < n; ++c) s = fma(J[(int64_t)c * ld + a], R[c], s);
+    S.jtr[a] = s;
+  }
+  __syncthreads();
+}
+
+// LU with partial pivoting on A = beta J'J + (mu+alpha) I; false on a zero pivot
+__device__ bool wide_solve(double* A, const double* jtj, int ld, int P, double alpha, double beta,
+                           double mu, WideSmem& S) {
+  const double damp = __dadd_rn(mu, alpha);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int a = warp; a < P; a += WWARPS)
+    for (int b = lane; b < P; b += 32) {
+      const double v = __dmul_rn(beta, jtj[(int64_t)a * ld + b]);
+      A[(int64_t)a * ld + b] = (a == b) ? __dadd_rn(v, damp) : v;
+    }
+  for (int a = threadIdx.x; a < P; a += WNT)
+    S.rhs[a] = -__dadd_rn(__dmul_rn(beta, S.jtr[a]), __dmul_rn(alpha, S.w[a]));
+  __syncthreads();
+  for (int k = 0; k < P; ++k) {
+    double best = -1.0;
+    int bi = k;
+    for (int i = k + threadIdx.x; i < P; i += WNT) {
+      const double v = fabs(A[(int64_t)i * ld + k]);
+      if (v > best) {
+        best = v;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, m);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, m);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      S.red[threadIdx.x >> 5] = best;
+      S.ired[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = S.red[0];
+      int p = S.ired[0];
+      for (int i = 1; i < WWARPS; ++i)
+        if (S.red[i] > b || (S.red[i] == b && S.ired[i] < p)) {
+          b = S.red[i];
+          p = S.ired[i];
+        }
+      S.piv = p;
+    }
+    __syncthreads();
+    const int p = S.piv;
+    if (A[(int64_t)p * ld + k] == 0.0) return false;
+    if (p != k) {
+      for (int j = threadIdx.x; j < P; j += WNT) {
+        const double t = A[(int64_t)k * ld + j];
+        A[(int64_t)k * ld + j] = A[(int64_t)p * ld + j];
+        A[(int64_t)p * ld + j] = t;
+      }
+      if (threadIdx.x == 0) {
+        const double t = S.rhs[k];
+        S.rhs[k] = S.rhs[p];
+        S.rhs[p] = t;
+      }
+      __syncthreads();
+    }
+    const double pk = A[(int64_t)k * ld + k];
+    const int m = P - k - 1;
+    for (int i = threadIdx.x; i < m; i += WNT) {
+      double* ai = A + (int64_t)(k + 1 + i) * ld;
+      ai[k] = __ddiv_rn(ai[k], pk);
+    }
+    __syncthreads();
+    // rank-1 update of the trailing block: warp = row, lanes = columns; four
+    // independent L2 loads in flight per lane (the update is L2-latency bound)
+    const double* __restrict__ rk = A + (int64_t)k * ld;
+    for (int i = k + 1 + warp; i < P; i += WWARPS) {
+      double* __restrict__ ai = A + (int64_t)i * ld;
+      const double l = ai[k];
+      int j = k + 1 + lane;
+      for (; j + 96 < P; j += 128) {
+        const double a0 = ai[j], a1 = ai[j + 32], a2 = ai[j + 64], a3 = ai[j + 96];
+        const double r0 = rk[j], r1 = rk[j + 32], r2 = rk[j + 64], r3 = rk[j + 96];
+        ai[j] = fma(-l, r0, a0);
+        ai[j + 32] = fma(-l, r1, a1);
+        ai[j + 64] = fma(-l, r2, a2);
+        ai[j + 96] = fma(-l, r3, a3);
+      }
+      for (; j < P; j += 32) ai[j] = fma(-l, rk[j], ai[j]);
+    }
+    __syncthreads();
+  }
+  for (int i = 0; i < P; ++i) {  // L y = Pb (unit lower)
+    double s = 0.0;
+    for (int j = threadIdx.x; j < i; j += WNT) s = fma(A[(int64_t)i * ld + j], S.rhs[j], s);
+    s = bsum(s, S);
+    if (threadIdx.x == 0) S.rhs[i] = __dsub_rn(S.rhs[i], s);
+    __syncthreads();
+  }
+  for (int i = P - 1; i >= 0; --i) {  // U x = y
+    double s = 0.0;
+    for (int j = i + 1 + threadIdx.x; j < P; j += WNT) s = fma(A[(int64_t)i * ld + j], S.delta[j], s);
+    s = bsum(s, S);
+    if (threadIdx.x == 0) S.delta[i] = __ddiv_rn(__dsub_rn(S.rhs[i], s), A[(int64_t)i * ld + i]);
+    __syncthreads();
+  }
+  return true;
+}
+
+// gamma = sum beta*l/(beta*l+alpha) over the eigenvalues of J'J (clipped at 0)
+__device__ double wide_gamma(double* A, const double* jtj, int ld, int P, double alpha, double beta,
+                             WideSmem& S) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int a = warp; a < P; a += WWARPS)
+    for (int b = lane; b < P; b += 32) A[(int64_t)a * ld + b] = jtj[(int64_t)a * ld + b];
+  __syncthreads();
+  for (int k = 0; k + 2 < P; ++k) {
+    double part = 0.0;
+    for (int i = k + 1 + threadIdx.x; i < P; i += WNT) {
+      const double xi = A[(int64_t)i * ld + k];
+      part = fma(xi, xi, part);
+    }
+    const double sig = bsum(part, S);
+    const double x0 = A[(int64_t)(k + 1) * ld + k];
+    const double tail = sig - x0 * x0;
+    if (!(tail > 0.0)) {
+      if (threadIdx.x == 0) S.ee[k] = x0;
+      __syncthreads();
+      continue;
+    }
+    const double al = x0 > 0.0 ? -sqrt(sig) : sqrt(sig);
+    const double bh = 1.0 / (sig - al * x0);
+    for (int i = k + 1 + threadIdx.x; i < P; i += WNT)
+      S.v[i] = A[(int64_t)i * ld + k] - (i == k + 1 ? al : 0.0);
+    __syncthreads();
+    for (int i = k + 1 + warp; i < P; i += WWARPS) {  // p = bh * A v (warp per row)
+      const double* __restrict__ ai = A + (int64_t)i * ld;
+      double p = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+      int j = k + 1 + lane;
+      for (; j + 96 < P; j += 128) {
+        p = fma(ai[j], S.v[j], p);
+        p1 = fma(ai[j + 32], S.v[j + 32], p1);
+        p2 = fma(ai[j + 64], S.v[j + 64], p2);
+        p3 = fma(ai[j + 96], S.v[j + 96], p3);
+      }
+      for (; j < P; j += 32) p = fma(ai[j], S.v[j], p);
+      p = (p + p1) + (p2 + p3);
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+      if (lane == 0) S.pv[i] = p * bh;
+    }
+    __syncthreads();
+    double kp = 0.0;
+    for (int i = k + 1 + threadIdx.x; i < P; i += WNT) kp = fma(S.v[i], S.pv[i], kp);
+    const double K = 0.5 * bh * bsum(kp, S);
+    for (int i = k + 1 + threadIdx.x; i < P; i += WNT) S.pv[i] = S.pv[i] - K * S.v[i];
+    __syncthreads();
+    for (int i = k + 1 + warp; i < P; i += WWARPS) {  // A -= v w' + w v'
+      double* __restrict__ ai = A + (int64_t)i * ld;
+      const double vi = S.v[i], wi = S.pv[i];
+      int j = k + 1 + lane;
+      for (; j + 96 < P; j += 128) {
+        const double a0 = ai[j], a1 = ai[j + 32], a2 = ai[j + 64], a3 = ai[j + 96];
+        ai[j] = a0 - fma(vi, S.pv[j], wi * S.v[j]);
+        ai[j + 32] = a1 - fma(vi, S.pv[j + 32], wi * S.v[j + 32]);
+        ai[j + 64] = a2 - fma(vi, S.pv[j + 64], wi * S.v[j + 64]);
+        ai[j + 96] = a3 - fma(vi, S.pv[j + 96], wi * S.v[j + 96]);
+      }
+      for (; j < P; j += 32) ai[j] -= fma(vi, S.pv[j], wi * S.v[j]);
+    }
+    if (threadIdx.x == 0) S.ee[k] = al;
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < P; i += WNT) S.dd[i] = A[(int64_t)i * ld + i];
+  if (threadIdx.x == 0 && P >= 2) S.ee[P - 2] = A[(int64_t)(P - 1) * ld + (P - 2)];
+  __syncthreads();
+  double glo = 1e308, ghi = -1e308, em = 0.0;
+  for (int i = threadIdx.x; i < P; i += WNT) {
+    if (i + 1 < P) S.e2[i] = S.ee[i] * S.ee[i];
+    const double r = (i > 0 ? fabs(S.ee[i - 1]) : 0.0) + (i + 1 < P ? fabs(S.ee[i]) : 0.0);
+    glo = fmin(glo, S.dd[i] - r);
+    ghi = fmax(ghi, S.dd[i] + r);
+    if (i + 1 < P) em = fmax(em, S.ee[i] * S.ee[i]);
+  }
+  glo = -bmax(-glo, S);
+  ghi = bmax(ghi, S);
+  em = bmax(em, S);
+  const double tnorm = fmax(fabs(glo), fabs(ghi));
+  const double eps = 2.220446049250313e-16;
+  const double pivmin = fmax(1e-300, em * 1e-300);
+  double part = 0.0;
+  for (int idx = threadIdx.x; idx < P; idx += WNT) {
+    double lo = glo - eps * tnorm - 1e-300, hi = ghi + eps * tnorm + 1e-300;
+    for (int it = 0; it < 120; ++it) {
+      // stop once the eigenvalue's gamma contribution beta*l/(beta*l+alpha) is
+      // pinned to 1e-13 (near-null eigenvalues, which decide gamma when alpha
+      // is tiny, are resolved far below alpha/beta), at relative precision, or
+      // when the interval is entirely <= 0 (clipped to 0)
+      if (hi <= 0.0 || hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 1e-290) break;
+      {
+        const double chi = beta * hi / (beta * hi + alpha);
+        const double clo = lo > 0.0 ? beta * lo / (beta * lo + alpha) : 0.0;
+        if (chi - clo <= 1e-13) break;
+      }
+      const double mid = 0.5 * (lo + hi);
+      int cnt = 0;
+      double q = S.dd[0] - mid;
+      if (fabs(q) < pivmin) q = -pivmin;
+      cnt += q < 0.0;
+      for (int j = 1; j < P; ++j) {
+        q = (S.dd[j] - mid) - S.e2[j - 1] / q;
+        if (fabs(q) < pivmin) q = -pivmin;
+        cnt += q < 0.0;
+      }
+      if (cnt > idx) hi = mid; else lo = mid;
+    }
+    const double lam = fmax(0.5 * (lo + hi), 0.0);
+    const double sc = __dmul_rn(beta, lam);
+    const double den = __dadd_rn(sc, alpha);
+    part += den > 0.0 ? __ddiv_rn(sc, den) : 0.0;
+  }
+  return bsum(part, S);
+}
+
+__global__ void __launch_bounds__(WNT) lm_wide_kernel(WideLaunch L) {
+  const int task = blockIdx.x;
+  if (task >= L.n_tasks) return;
+  __shared__ WideSmem S;
+  const bbml_lm_task tk = L.tasks[task];
+  const int orig = L.orig_index[task];
+  const int n = tk.n, d = tk.d, h = tk.h;
+  const int P = h * (d + 2) + 1;
+  const int ld = L.ld, xs = L.x_stride;
+  const double* X = L.X + tk.row_begin * (int64_t)xs;
+  const double* Y = L.y + tk.row_begin;
+  double* slab = L.scratch + (int64_t)blockIdx.x * L.slab_doubles;
+  double* jtj = slab;
+  double* A = jtj + (int64_t)ld * ld;
+  double* R = A + (int64_t)ld * ld;
+  double* J = R + ((n + 3) & ~3);
+
+  if (threadIdx.x == 0) {
+    Pcg64 rng;
+    rng.seed(tk.seed);
+    const double s1 = __ddiv_rn(1.0, __dsqrt_rn((double)d));
+    const double s2 = __ddiv_rn(1.0, __dsqrt_rn((double)h));
+    const int hd = h * d;
+    for (int i = 0; i < hd + h; ++i) S.w[i] = rng.uniform(-s1, s1);
+    for (int i = hd + h; i < P; ++i) S.w[i] = rng.uniform(-s2, s2);
+  }
+  __syncthreads();
+  double alpha = tk.alpha0, beta = tk.beta0, mu = tk.mu0;
+  const bool est = tk.estimate != 0;
+  double* hist = (tk.hist_offset >= 0) ? L.history + tk.hist_offset : nullptr;
+  double e_d = wide_energy(S.w, X, Y, n, d, h, xs, S);
+  double e_w = 0.0;
+  for (int i = 0; i < P; ++i) e_w = fma(S.w[i], S.w[i], e_w);
+  bool have_stats = false;
+  int code = BBML_MODEL_OK, trials = 0, epochs = 0, any_pinned = 0, stable = 0;
+  double fail_mu = 0.0, last_mu = NAN, last_gamma = NAN, prev_g = 0.0, prev_d = 0.0, prev_w = 0.0;
+  bool have_prev = false;
+
+  for (int ep = 0; ep < tk.max_epochs; ++ep) {
+    if (!have_stats) wide_stats(J, R, jtj, ld, X, Y, n, d, h, P, xs, S);
+    const double f0 = __dadd_rn(__dmul_rn(beta, e_d), __dmul_rn(alpha, e_w));
+    bool accepted = false;
+    double td = 0.0, tw = 0.0;
+    while (true) {
+      ++trials;
+      if (!wide_solve(A, jtj, ld, P, alpha, beta, mu, S)) {
+        code = BBML_MODEL_SINGULAR;
+        fail_mu = mu;
+        break;
+      }
+      for (int i = threadIdx.x; i < P; i += WNT) S.wt[i] = __dadd_rn(S.w[i], S.delta[i]);
+      __syncthreads();
+      td = wide_energy(S.wt, X, Y, n, d, h, xs, S);
+      tw = 0.0;
+      for (int i = 0; i < P; ++i) tw = fma(S.wt[i], S.wt[i], tw);
+      const double f1 = __dadd_rn(__dmul_rn(beta, td), __dmul_rn(alpha, tw));
+      if (f1 < f0) {
+        mu = fmax(__dmul_rn(mu, tk.mu_dec), 1e-20);
+        accepted = true;
+        break;
+      }
+      mu = __dmul_rn(mu, tk.mu_inc);
+      if (mu > tk.mu_max) break;
+    }
+    if (code != BBML_MODEL_OK || !accepted) break;
+    __syncthreads();
+    for (int i = threadIdx.x; i < P; i += WNT) S.w[i] = S.wt[i];
+    __syncthreads();
+    e_d = td;
+    e_w = tw;
+    const double f1 = __dadd_rn(__dmul_rn(beta, e_d), __dmul_rn(alpha, e_w));
+    double gamma = NAN;
+    int pinned = 0;
+    if (est) {
+      wide_stats(J, R, jtj, ld, X, Y, n, d, h, P, xs, S);
+      have_stats = true;
+      gamma = wide_gamma(A, jtj, ld, P, alpha, beta, S);
+      double na, nb;
+      if (e_w > 0.0) {
+        na = __ddiv_rn(gamma, __dmul_rn(2.0, e_w));
+      } else {
+        na = 1e12;
+        pinned = 1;
+      }
+      if (e_d > 0.0) {
+        nb = __ddiv_rn(__dsub_rn((double)n, gamma), __dmul_rn(2.0, e_d));
+      } else {
+        nb = 1e12;
+        pinned = 1;
+      }
+      alpha = fmin(fmax(na, 1e-12), 1e12);
+      beta = fmin(fmax(nb, 1e-12), 1e12);
+    } else {
+      have_stats = false;
+    }
+    any_pinned |= pinned;
+    last_mu = mu;
+    last_gamma = gamma;
+    epochs = ep + 1;
+    if (hist && threadIdx.x == 0) {
+      double* r = hist + (int64_t)ep * 10;
+      r[0] = ep; r[1] = f0; r[2] = f1; r[3] = e_d; r[4] = e_w;
+      r[5] = alpha; r[6] = beta; r[7] = gamma; r[8] = mu; r[9] = pinned;
+    }
+    if (have_prev && est) {
+      const bool ok = fabs(gamma - prev_g) <= 1e-7 * fmax(fabs(prev_g), 1e-300) &&
+                      fabs(e_d - prev_d) <= 1e-7 * fmax(fabs(prev_d), 1e-300) &&
+                      fabs(e_w - prev_w) <= 1e-7 * fmax(fabs(prev_w), 1e-300);
+      if (ok) {
+        if (++stable >= 5) break;
+      } else {
+        stable = 0;
+      }
+    }
+    prev_g = gamma;
+    prev_d = e_d;
+    prev_w = e_w;
+    have_prev = true;
+  }
+  __syncthreads();
+  double* W = L.weights + tk.w_offset;
+  for (int i = threadIdx.x; i < P; i += WNT) W[i] = S.w[i];
+  if (threadIdx.x == 0) {
+    bbml_model_status st{};
+    st.code = code;
+    st.epochs = epochs;
+    st.detail = any_pinned;
+    st.trials = trials;
+    st.value = fail_mu;
+    st.mu = last_mu;
+    st.gamma = last_gamma;
+    st.alpha = alpha;
+    st.beta = beta;
+    L.status[orig] = st;
+  }
+}
+
+// Launch all wide tasks (P > 32) of one lm_train call on `s`; tasks/orig are
+// device arrays (already sorted); scratch slabs are stream-ordered.
+bbml_status lm_wide_launch(const bbml_lm_task* d_tasks, const int32_t* d_orig,
+                           const bbml_lm_task* h_tasks, int32_t n_tasks, const double* X,
+                           const double* y, int32_t x_stride, double* weights, double* history,
+                           bbml_model_status* status, ScratchBuffer& scratch, cudaStream_t s,
+                           bool alloc_only, double** slabs) {
+  if (n_tasks == 0) return BBML_OK;
+  int pmax = 0, nmax = 0;
+  for (int i = 0; i < n_tasks; ++i) {
+    pmax = std::max(pmax, h_tasks[i].h * (h_tasks[i].d + 2) + 1);
+    nmax = std::max(nmax, h_tasks[i].n);
+  }
+  const int ld = (pmax + 3) & ~3;
+  const int64_t slab = 2 * (int64_t)ld * ld + ((nmax + 3) & ~3) + (int64_t)nmax * ld;
+  if (alloc_only) return scratch.alloc(slabs, slab * n_tasks);
+  double* d_scratch = *slabs;
+  WideLaunch L{};
+  L.tasks = d_tasks;
+  L.orig_index = d_orig;
+  L.n_tasks = n_tasks;
+  L.x_stride = x_stride;
+  L.X = X;
+  L.y = y;
+  L.weights = weights;
+  L.history = history;
+  L.status = status;
+  L.scratch = d_scratch;
+  L.slab_doubles = slab;
+  L.ld = ld;
+  lm_wide_kernel<<<n_tasks, WNT, 0, s>>>(L);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BBML_OK : cuda_status(e, "lm_wide launch");
+}
+
+}  // namespace bbml
