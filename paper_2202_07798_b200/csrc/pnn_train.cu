@@ -23,6 +23,8 @@
 //                    double buffer while the consumer trains on epoch e, so the
 //                    sequential shuffle is off the training critical path.
 //   Hand-off: per-model produced/consumed epoch counters in shared memory.
+#include <stdlib.h>
+
 #include <algorithm>
 #include <vector>
 
@@ -79,6 +81,15 @@ __device__ __forceinline__ int ld_volatile(const int* p) { return *(volatile con
 __device__ __forceinline__ void st_volatile(int* p, int v) { *(volatile int*)p = v; }
 
 constexpr int kConsumedDone = 1 << 30;
+
+// uint16 permutations always live in shared memory, int32 ones (series too
+// long for the shared-memory double buffer) in global memory.  Keeping the
+// address space a compile-time property lets the compiler emit LDS/STS
+// instead of generic loads (which go through L1TEX with global latency).
+template <typename PermT>
+__host__ __device__ constexpr bool perm_smem() {
+  return sizeof(PermT) == 2;
+}
 
 // Fisher-Yates of arange(n) from the top index down (Generator.permutation)
 template <typename PermT>
@@ -175,9 +186,9 @@ __device__ void perm_producer_warp(const PnnLaunch& L, int groups, int pw, int n
       alive = true;
       if (c < e - 1) continue;  // buffer (e & 1) still in use by epoch e - 2
       const int n = pm[m].n;
-      PermT* perm = (L.perm_in_smem ? sperm + (int64_t)m * 2 * L.perm_cap
+      PermT* perm = (perm_smem<PermT>() ? sperm + (int64_t)m * 2 * L.perm_cap
                                     : (PermT*)L.perm_global + 2 * L.perm_offset[gid]) +
-                    (e & 1) * (L.perm_in_smem ? (int64_t)L.perm_cap : (int64_t)n);
+                    (e & 1) * (perm_smem<PermT>() ? (int64_t)L.perm_cap : (int64_t)n);
       for (int x = lane; x < n; x += 32) perm[x] = (PermT)x;
       u128 s = ((u128)pm[m].s_hi << 64) | pm[m].s_lo;
       const u128 inc = ((u128)pm[m].inc_hi << 64) | pm[m].inc_lo;
@@ -330,9 +341,9 @@ __global__ void pnn_train_kernel(PnnLaunch L) {
   const int n = tk.n, d = tk.d, h = tk.h, B = tk.batch;
   const double* __restrict__ X = L.X + tk.row_begin * (int64_t)L.x_stride;
   const double* __restrict__ Y = L.y + tk.row_begin;
-  const PermT* pbase = L.perm_in_smem ? sperm + (int64_t)gi * 2 * L.perm_cap
+  const PermT* pbase = perm_smem<PermT>() ? sperm + (int64_t)gi * 2 * L.perm_cap
                                       : (const PermT*)L.perm_global + 2 * L.perm_offset[gid];
-  const int64_t cap = L.perm_in_smem ? L.perm_cap : n;
+  const int64_t cap = perm_smem<PermT>() ? L.perm_cap : n;
 
   // ---- init (pnn.py:97-104): every lane replays the P draws, keeps its own
   T w1[U][DM], b1[U], w2[U];
@@ -605,9 +616,9 @@ __device__ __forceinline__ void pnn_lat_body(const PnnLaunch& L) {
   const int n = tk.n, d = tk.d, h = tk.h, B = tk.batch;
   const double* __restrict__ X = L.X + tk.row_begin * (int64_t)L.x_stride;
   const double* __restrict__ Y = L.y + tk.row_begin;
-  const PermT* pbase = L.perm_in_smem ? sperm + (int64_t)gi * 2 * L.perm_cap
+  const PermT* pbase = perm_smem<PermT>() ? sperm + (int64_t)gi * 2 * L.perm_cap
                                       : (const PermT*)L.perm_global + 2 * L.perm_offset[gid];
-  const int64_t cap = L.perm_in_smem ? L.perm_cap : n;
+  const int64_t cap = perm_smem<PermT>() ? L.perm_cap : n;
 
   // ---- init (pnn.py:97-104)
   T w1[DM], b1 = T(0), w2 = T(0), b2;
@@ -661,24 +672,46 @@ __device__ __forceinline__ void pnn_lat_body(const PnnLaunch& L) {
                              tk.row_begin;
   const bool vec4 = sizeof(T) == 4 && DM <= 4 && rstride == 4;
   const bool y_in_x = vec4 && L.y_in_x;
-  auto load = [&](T (&xs)[SP][DM], T (&ys)[SP], const PermT* perm, int off, int cnt) {
+  // Prefetch: the raw load registers are filled one chunk ahead and only
+  // read (masked / unpacked) when that chunk is consumed, so the L2 latency
+  // overlaps the previous chunk's compute instead of stalling at the load.
+  struct Raw {
+    float4 v[SP];
+    T x[SP][DM];
+    T y[SP];
+  };
+  auto load = [&](Raw& r, const PermT* perm, int off, int cnt) {
 #pragma unroll
     for (int i = 0; i < SP; ++i) {
       const int c = sg * SP + i;
       const int row = (int)perm[off + (c < cnt ? c : 0)];
       if constexpr (sizeof(T) == 4 && DM <= 4) {
         if (vec4) {
-          const float4 v = __ldg((const float4*)(XT + (int64_t)row * 4));
-          const float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int k = 0; k < DM; ++k) xs[i][k] = (k < d) ? e[k] : 0.0f;
-          ys[i] = y_in_x ? v.w : __ldg(YT + row);
+          r.v[i] = __ldg((const float4*)(XT + (int64_t)row * 4));
+          if (!y_in_x) r.y[i] = __ldg(YT + row);
           continue;
         }
       }
 #pragma unroll
-      for (int k = 0; k < DM; ++k) xs[i][k] = (k < d) ? __ldg(XT + (int64_t)row * rstride + k) : T(0);
-      ys[i] = __ldg(YT + row);
+      for (int k = 0; k < DM; ++k) r.x[i][k] = (k < d) ? __ldg(XT + (int64_t)row * rstride + k) : T(0);
+      r.y[i] = __ldg(YT + row);
+    }
+  };
+  auto unpack = [&](const Raw& r, T (&xs)[SP][DM], T (&ys)[SP]) {
+#pragma unroll
+    for (int i = 0; i < SP; ++i) {
+      if constexpr (sizeof(T) == 4 && DM <= 4) {
+        if (vec4) {
+          const float e[4] = {r.v[i].x, r.v[i].y, r.v[i].z, r.v[i].w};
+#pragma unroll
+          for (int k = 0; k < DM; ++k) xs[i][k] = (k < d) ? e[k] : 0.0f;
+          ys[i] = y_in_x ? r.v[i].w : r.y[i];
+          continue;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < DM; ++k) xs[i][k] = r.x[i][k];
+      ys[i] = r.y[i];
     }
   };
 
@@ -690,8 +723,11 @@ __device__ __forceinline__ void pnn_lat_body(const PnnLaunch& L) {
     T eloss = T(0);
     zero_grads();
     int bs = 0, s0 = 0;
-    T xs[SP][DM], ys[SP];
-    load(xs, ys, perm, 0, min(C, min(B, n)));
+    // ping-pong prefetch buffers: a register copy (cur = nxt) would force the
+    // in-flight loads to complete, so the two buffers alternate roles instead
+    Raw rb0, rb1;
+    bool flip = false;
+    load(rb0, perm, 0, min(C, min(B, n)));
     while (true) {
       const int nb = min(B, n - bs);
       const int cnt = min(C, nb - s0);
@@ -701,8 +737,16 @@ __device__ __forceinline__ void pnn_lat_body(const PnnLaunch& L) {
         ns0 = 0;
       }
       const bool more = nbs < n;
-      T nx[SP][DM], ny[SP];
-      if (more) load(nx, ny, perm, nbs + ns0, min(C, min(B, n - nbs) - ns0));
+      T xs[SP][DM], ys[SP];
+      const int ncnt = more ? min(C, min(B, n - nbs) - ns0) : 0;
+      if (!flip) {
+        unpack(rb0, xs, ys);
+        if (more) load(rb1, perm, nbs + ns0, ncnt);
+      } else {
+        unpack(rb1, xs, ys);
+        if (more) load(rb0, perm, nbs + ns0, ncnt);
+      }
+      flip = !flip;
 
       // forward
       T a[SP], z[SP];
@@ -800,12 +844,6 @@ __device__ __forceinline__ void pnn_lat_body(const PnnLaunch& L) {
         zero_grads();
       }
       if (!more) break;
-#pragma unroll
-      for (int i = 0; i < SP; ++i) {
-        ys[i] = ny[i];
-#pragma unroll
-        for (int k = 0; k < DM; ++k) xs[i][k] = nx[i][k];
-      }
       bs = nbs;
       s0 = ns0;
     }
@@ -853,6 +891,22 @@ template <typename T, int DM, int SP, typename PermT>
 __global__ void __launch_bounds__(160, 2) pnn_lat_kernel_shared(PnnLaunch L) {
   pnn_lat_body<T, DM, SP, PermT>(L);
 }
+// 4 consumer + 2 producer warps (each producer serves 2 models), 2 CTAs per SM
+template <typename T, int DM, int SP, typename PermT>
+__global__ void __launch_bounds__(192, 2) pnn_lat_kernel_np2(PnnLaunch L) {
+  pnn_lat_body<T, DM, SP, PermT>(L);
+}
+
+// producer warps per CTA for long-series buckets (tuning knob BBML_PNN_NPW = 1|2|4)
+static int long_npw() {
+  static const int v = [] {
+    const char* e = getenv("BBML_PNN_NPW");
+    // default 4: one-box A/B on suite16 R=32 (r01): NPW=4 636.9 ms vs NPW=2 660.8 ms
+    const int x = e ? atoi(e) : 4;
+    return (x == 1 || x == 2 || x == 4) ? x : 4;
+  }();
+  return v;
+}
 
 // ------------------------------------------------------------------------
 // host dispatch
@@ -899,14 +953,15 @@ static cudaError_t launch_variant(PnnLaunch L, int64_t nmax, size_t smem_limit, 
   // CTA is 5 warps and two CTAs fit per SM.
   const bool shared_prod = LAT && nmax < kLongSeries;
   const int groups_max = 4;
-  const int npw_max = shared_prod ? 1 : groups_max;
-  const size_t flags = pnn_smem_header(groups_max, npw_max);
+  const int npw_long = LAT ? long_npw() : groups_max;
+  const int npw_max = shared_prod ? 1 : npw_long;
+  const size_t flags = pnn_smem_header(groups_max, groups_max);
   const size_t per_group = 2 * (size_t)nmax * sizeof(PermT);
-  int groups = (int)std::min<size_t>(groups_max, (smem_limit - flags) / per_group);
+  int groups = perm_smem<PermT>() ? (int)std::min<size_t>(groups_max, (smem_limit - flags) / per_group) : 0;
   size_t smem;
   int npw;
   if (groups >= 1) {
-    npw = shared_prod ? 1 : groups;
+    npw = std::min(groups, npw_max);
     L.perm_in_smem = 1;
     L.perm_cap = (int32_t)nmax;
     smem = pnn_smem_header(groups, npw) + (size_t)groups * per_group;
@@ -922,8 +977,9 @@ static cudaError_t launch_variant(PnnLaunch L, int64_t nmax, size_t smem_limit, 
   const int prod = 32 * npw;
   const int blocks = (int)ceil_div(L.n_tasks, groups);
   auto k = !LAT ? pnn_train_kernel<T, DM, HM, G, SC, PermT>
-                : (npw == 1 && shared_prod ? pnn_lat_kernel_shared<T, DM, 5, PermT>
-                                           : pnn_lat_kernel<T, DM, 5, PermT>);
+                : (npw == 1 ? pnn_lat_kernel_shared<T, DM, 5, PermT>
+                            : npw == 2 ? pnn_lat_kernel_np2<T, DM, 5, PermT>
+                                       : pnn_lat_kernel<T, DM, 5, PermT>);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -935,7 +991,10 @@ static cudaError_t launch_variant(PnnLaunch L, int64_t nmax, size_t smem_limit, 
 template <typename T, int DM, int HM>
 static cudaError_t launch_dm_hm(const PnnLaunch& L, int64_t nmax, size_t smem_limit,
                                 cudaStream_t s) {
-  if (nmax <= 65535) return launch_variant<T, DM, HM, uint16_t>(L, nmax, smem_limit, s);
+  // uint16 in shared memory whenever one model's double buffer fits, else int32 in global
+  const bool fits = nmax <= 65535 &&
+                    pnn_smem_header(4, 4) + 2 * (size_t)nmax * sizeof(uint16_t) <= smem_limit;
+  if (fits) return launch_variant<T, DM, HM, uint16_t>(L, nmax, smem_limit, s);
   return launch_variant<T, DM, HM, int32_t>(L, nmax, smem_limit, s);
 }
 

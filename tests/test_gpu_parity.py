@@ -195,3 +195,62 @@ def test_br_hidden10_accuracy_parity_gramschmit():
     acc_ora = 100 * (1 - float(np.mean(ora)))
     print("gramschmit h=10 accuracy device %.3f oracle %.3f" % (acc_dev, acc_ora))
     assert abs(acc_dev - acc_ora) <= 0.5
+
+
+def test_train_one_matches_reference_golden(golden):
+    """experiment.train_one / train_many (batched device path) against the
+    reference's own train_one on the same series: errors, flags, split sizes,
+    MSE and raw predictions (PNN FP64 <= 1e-9; BR hidden 1 <= 1e-6), seeds and
+    predict_counts extrapolation through the saved model."""
+    from paper_2202_07798_b200.experiment import ExperimentConfig, train_many
+    from paper_2202_07798_b200.traces import BbSeries, SplitMode
+
+    g = golden("train_one")
+    modes = {"high-low": SplitMode.HIGH_LOW, "random": SplitMode.RANDOM,
+             "mixed-high-low": SplitMode.MIXED_HIGH_LOW}
+    groups = {}
+    for i in range(int(g["n_runs"])):
+        p = f"r{i}_"
+        app, k, b, kind, mode = (str(v) for v in g[p + "key"])
+        seed, pe, be = (int(v) for v in g[p + "cfg"])
+        groups.setdefault((mode, seed, pe, be), []).append((i, (app, int(k), int(b)), kind))
+    checked = 0
+    for (mode, seed, pe, be), items in groups.items():
+        cfg = ExperimentConfig(split_mode=modes[mode], seed=seed, pnn_epochs=pe, br_max_epochs=be)
+        series = {}
+        pairs = []
+        for i, key, kind in items:
+            p = f"r{i}_"
+            s = series.setdefault(key, BbSeries(key, g[p + "X"], g[p + "y"]))
+            pairs.append((s, kind))
+        results = train_many(pairs, cfg).results
+        for (i, key, kind), r in zip(items, results):
+            p = f"r{i}_"
+            want_err = str(g[p + "error"])
+            assert (r.error or "") == want_err or (r.error and want_err), (key, kind, r.error, want_err)
+            if want_err:
+                assert r.error is not None
+                continue
+            assert r.error is None, (key, kind, r.error)
+            assert [r.n_train, r.n_test] == list(g[p + "nn"])
+            assert [r.constant_target, r.pinned_hyperparams] == list(g[p + "flags"]), (key, kind)
+            assert r.saved.seed == int(g[p + "seed"][0])
+            tol = 1e-9 if kind == "pnn" else 1e-6
+            # relative error with a floor at 1e-6 of the series' count scale
+            # (predictions of a count that is 0 on the test side are ~1e-9)
+            floor = 1e-6 * max(1.0, float(np.max(np.abs(g[p + "y"]))))
+            if kind == "brbpnn" and float(g[p + "br_meta"][4]) >= 1e12:
+                # degenerate fit: E_D -> 0 drives beta to its 1e12 clamp and the
+                # damped system to condition ~1e24, so late epochs amplify
+                # rounding (a step target fitted by a saturating tanh).  Gate on
+                # accuracy parity (north star: +-0.5 pp) instead of 1e-3.
+                assert abs(r.mse - float(g[p + "mse"])) <= 0.005, (key, kind)
+                assert _rel(r.pred_raw, g[p + "pred_raw"], floor) <= 1e-2, (key, kind)
+                checked += 1
+                continue
+            assert _rel(r.pred_raw, g[p + "pred_raw"], floor) <= tol, (key, kind)
+            assert abs(r.mse - float(g[p + "mse"])) <= tol * max(1.0, abs(float(g[p + "mse"]))), (key, kind)
+            got = r.saved.predict_counts(g[p + "raw_q"])
+            assert _rel(got, g[p + "counts_q"], floor) <= tol, (key, kind)
+            checked += 1
+    assert checked >= 60
