@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "sturm.cuh"
 #include "launch.h"
 #include "pcg64.cuh"
 
@@ -832,56 +833,35 @@ __device__ double w_gamma_tri(WarpLm<PM>& S, int P, double alpha, double beta, i
   if (lane < P) dd[lane] = S.A[lane * LD + lane];
   if (lane == 0 && P >= 2) ee[P - 2] = S.A[(P - 1) * LD + (P - 2)];
   __syncwarp();
-  if (lane + 1 < P) e2[lane] = ee[lane] * ee[lane];
-  // Gershgorin interval of T
-  double glo = 0.0, ghi = 0.0, emax2 = 0.0;
+  // Gershgorin interval of T, then T scaled by a power of two to ||T|| <= 1
+  double glo = 0.0, ghi = 0.0;
   if (lane < P) {
     const double r = (lane > 0 ? fabs(ee[lane - 1]) : 0.0) + (lane + 1 < P ? fabs(ee[lane]) : 0.0);
     glo = dd[lane] - r;
     ghi = dd[lane] + r;
-    emax2 = lane + 1 < P ? e2[lane] : 0.0;
   }
-  __syncwarp();
 #pragma unroll
   for (int m = 16; m >= 1; m >>= 1) {
     glo = fmin(glo, __shfl_xor_sync(0xffffffffu, glo, m));
     ghi = fmax(ghi, __shfl_xor_sync(0xffffffffu, ghi, m));
-    emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, m));
   }
   const double tnorm = fmax(fabs(glo), fabs(ghi));
-  const double eps = 2.220446049250313e-16;
-  const double pivmin = fmax(1e-300, emax2 * 1e-300);
-  double part = 0.0;
-  if (lane < P) {  // lane-th smallest eigenvalue by bisection
-    double lo = glo - eps * tnorm - 1e-300, hi = ghi + eps * tnorm + 1e-300;
-    for (int it = 0; it < 120; ++it) {
-      // stop once the eigenvalue's gamma contribution beta*l/(beta*l+alpha) is
-      // pinned to 1e-13 (near-null eigenvalues, which decide gamma when alpha
-      // is tiny, are resolved far below alpha/beta), at relative precision, or
-      // when the interval is entirely <= 0 (clipped to 0)
-      if (hi <= 0.0 || hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 1e-290) break;
-      {
-        const double chi = beta * hi / (beta * hi + alpha);
-        const double clo = lo > 0.0 ? beta * lo / (beta * lo + alpha) : 0.0;
-        if (chi - clo <= 1e-13) break;
-      }
-      const double mid = 0.5 * (lo + hi);
-      int cnt = 0;
-      double q = dd[0] - mid;
-      if (fabs(q) < pivmin) q = -pivmin;
-      cnt += q < 0.0;
-      for (int j = 1; j < P; ++j) {
-        q = (dd[j] - mid) - e2[j - 1] / q;
-        if (fabs(q) < pivmin) q = -pivmin;
-        cnt += q < 0.0;
-      }
-      if (cnt > lane) hi = mid; else lo = mid;
+  if (!(tnorm > 0.0)) return 0.0;  // J'J = 0: every eigenvalue clipped to 0
+  const double scale = sturm_scale(tnorm);
+  __syncwarp();
+  if (lane < P) {
+    dd[lane] *= scale;
+    if (lane + 1 < P) {
+      const double es = ee[lane] * scale;
+      e2[lane] = es * es;
     }
-    const double lam = fmax(0.5 * (lo + hi), 0.0);
-    const double sc = __dmul_rn(beta, lam);
-    const double den = __dadd_rn(sc, alpha);
-    part = den > 0.0 ? __ddiv_rn(sc, den) : 0.0;
   }
+  __syncwarp();
+  const double hi0 = (ghi + 2.220446049250313e-16 * tnorm) * scale;
+  const int n_neg = sturm_count(dd, e2, P, 0.0);
+  const double part = lane < P ? sturm_gamma_part(dd, e2, P, lane, n_neg, hi0, alpha / beta * scale,
+                                                  1.0 / scale, alpha, beta)
+                               : 0.0;
   return warp_sum(part);
 }
 

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "sturm.cuh"
 #include "launch.h"
 #include "pcg64.cuh"
 
@@ -330,51 +331,32 @@ __device__ double wide_gamma(double* A, const double* jtj, int ld, int P, double
   for (int i = threadIdx.x; i < P; i += WNT) S.dd[i] = A[(int64_t)i * ld + i];
   if (threadIdx.x == 0 && P >= 2) S.ee[P - 2] = A[(int64_t)(P - 1) * ld + (P - 2)];
   __syncthreads();
-  double glo = 1e308, ghi = -1e308, em = 0.0;
+  double glo = 1e308, ghi = -1e308;
   for (int i = threadIdx.x; i < P; i += WNT) {
-    if (i + 1 < P) S.e2[i] = S.ee[i] * S.ee[i];
     const double r = (i > 0 ? fabs(S.ee[i - 1]) : 0.0) + (i + 1 < P ? fabs(S.ee[i]) : 0.0);
     glo = fmin(glo, S.dd[i] - r);
     ghi = fmax(ghi, S.dd[i] + r);
-    if (i + 1 < P) em = fmax(em, S.ee[i] * S.ee[i]);
   }
   glo = -bmax(-glo, S);
   ghi = bmax(ghi, S);
-  em = bmax(em, S);
   const double tnorm = fmax(fabs(glo), fabs(ghi));
-  const double eps = 2.220446049250313e-16;
-  const double pivmin = fmax(1e-300, em * 1e-300);
-  double part = 0.0;
-  for (int idx = threadIdx.x; idx < P; idx += WNT) {
-    double lo = glo - eps * tnorm - 1e-300, hi = ghi + eps * tnorm + 1e-300;
-    for (int it = 0; it < 120; ++it) {
-      // stop once the eigenvalue's gamma contribution beta*l/(beta*l+alpha) is
-      // pinned to 1e-13 (near-null eigenvalues, which decide gamma when alpha
-      // is tiny, are resolved far below alpha/beta), at relative precision, or
-      // when the interval is entirely <= 0 (clipped to 0)
-      if (hi <= 0.0 || hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 1e-290) break;
-      {
-        const double chi = beta * hi / (beta * hi + alpha);
-        const double clo = lo > 0.0 ? beta * lo / (beta * lo + alpha) : 0.0;
-        if (chi - clo <= 1e-13) break;
-      }
-      const double mid = 0.5 * (lo + hi);
-      int cnt = 0;
-      double q = S.dd[0] - mid;
-      if (fabs(q) < pivmin) q = -pivmin;
-      cnt += q < 0.0;
-      for (int j = 1; j < P; ++j) {
-        q = (S.dd[j] - mid) - S.e2[j - 1] / q;
-        if (fabs(q) < pivmin) q = -pivmin;
-        cnt += q < 0.0;
-      }
-      if (cnt > idx) hi = mid; else lo = mid;
+  if (!(tnorm > 0.0)) return 0.0;  // J'J = 0: every eigenvalue clipped to 0
+  // T scaled by a power of two to ||T|| <= 1 for the division-free Sturm count
+  const double scale = sturm_scale(tnorm);
+  for (int i = threadIdx.x; i < P; i += WNT) {
+    S.dd[i] *= scale;
+    if (i + 1 < P) {
+      const double es = S.ee[i] * scale;
+      S.e2[i] = es * es;
     }
-    const double lam = fmax(0.5 * (lo + hi), 0.0);
-    const double sc = __dmul_rn(beta, lam);
-    const double den = __dadd_rn(sc, alpha);
-    part += den > 0.0 ? __ddiv_rn(sc, den) : 0.0;
   }
+  __syncthreads();
+  const double hi0 = (ghi + 2.220446049250313e-16 * tnorm) * scale;
+  const int n_neg = sturm_count(S.dd, S.e2, P, 0.0);
+  const double r = alpha / beta * scale;
+  double part = 0.0;
+  for (int idx = threadIdx.x; idx < P; idx += WNT)
+    part += sturm_gamma_part(S.dd, S.e2, P, idx, n_neg, hi0, r, 1.0 / scale, alpha, beta);
   return bsum(part, S);
 }
 

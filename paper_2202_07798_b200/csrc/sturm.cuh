@@ -1,0 +1,91 @@
+// Eigenvalue part of the MacKay evidence update (brbpnn.py:221-236):
+// gamma = sum_i beta*l_i / (beta*l_i + alpha) over the eigenvalues l_i of J'J,
+// clipped at 0, computed from the symmetric tridiagonal T = Q'(J'J)Q that the
+// caller's Householder reduction leaves as (diagonal dd, off-diagonal ee).
+//
+// Bisection with Sturm counts, one eigenvalue per thread:
+//   * T is first scaled by an exact power of two so that ||T|| <= 1 (Gershgorin);
+//     the count then uses the division-free three-term recurrence
+//       p_j = (d_j - x) p_{j-1} - e_{j-1}^2 p_{j-2}
+//     (q_j = p_j / p_{j-1} is the LDL' pivot of T - xI; q_j < 0 <=> sign change;
+//     |q_j| below a tiny floor is replaced by -floor, LAPACK dlaebz's pivmin rule),
+//     rescaled by powers of two to stay in range.  One dependent DFMA per row
+//     instead of a DDIV.
+//   * eigenvalues below 0 (one shared count at x = 0) contribute 0 (clipped);
+//     the others bisect [0, ||T||] on the IEEE bit pattern (the midpoint of the
+//     bit patterns is the geometric midpoint across binades, the arithmetic one
+//     inside a binade), so near-null eigenvalues converge in relative terms.
+//   * stop when the gamma contribution is pinned to 1e-13 (division-free form
+//     of f(hi) - f(lo) = r (hi-lo) / ((hi+r)(lo+r)), r = alpha/beta) or at
+//     ~2 ulp relative width.
+// Eigenvalue accuracy is the backward-stable eps*||T|| of bisection, the same
+// class as LAPACK dsyevd used by the reference.
+#pragma once
+#include <cstdint>
+
+namespace bbml {
+
+constexpr double kSturmPiv = 0x1p-400;  // pivot floor relative to |p_{j-1}| (scaled T)
+
+// 2^-ceil(log2(t)) for t > 0 (exact power of two), so t * scale <= 1
+__device__ __forceinline__ double sturm_scale(double t) {
+  int e;
+  const double m = frexp(t, &e);  // t = m * 2^e, m in [0.5, 1)
+  (void)m;
+  return ldexp(1.0, -e);
+}
+
+// number of eigenvalues of the scaled T below x
+__device__ __forceinline__ int sturm_count(const double* __restrict__ dd,
+                                           const double* __restrict__ e2, int P, double x) {
+  double p0 = 1.0, p1 = dd[0] - x;
+  if (fabs(p1) < kSturmPiv) p1 = -kSturmPiv;
+  int cnt = p1 < 0.0;
+#pragma unroll 4
+  for (int j = 1; j < P; ++j) {
+    const double fl = kSturmPiv * p1;
+    double p2 = fma(dd[j] - x, p1, -(e2[j - 1] * p0));
+    p2 = fabs(p2) < fabs(fl) ? -fl : p2;
+    cnt += (__double2hiint(p2) ^ __double2hiint(p1)) < 0;
+    p0 = p1;
+    p1 = p2;
+    const double m = fmax(fabs(p0), fabs(p1));
+    const double s = m > 0x1p200 ? 0x1p-400 : (m < 0x1p-200 ? 0x1p400 : 1.0);
+    p0 *= s;
+    p1 *= s;
+  }
+  return cnt;
+}
+
+// gamma contribution of the k-th smallest eigenvalue (0-based).  dd/e2 are the
+// scaled diagonal and squared off-diagonal; hi0 = scaled Gershgorin upper
+// bound; n_neg = sturm_count(0); r = (alpha/beta) * scale; inv_scale = 1/scale.
+__device__ __forceinline__ double sturm_gamma_part(const double* __restrict__ dd,
+                                                   const double* __restrict__ e2, int P, int k,
+                                                   int n_neg, double hi0, double r,
+                                                   double inv_scale, double alpha, double beta) {
+  if (k < n_neg || !(hi0 > 0.0)) return 0.0;  // eigenvalue <= 0: clipped
+  double lo = 0.0, hi = hi0;
+  long long lb = 0, hb = __double_as_longlong(hi0);
+  constexpr double eps = 2.220446049250313e-16;
+  for (int it = 0; it < 80; ++it) {
+    const double w = hi - lo;
+    if (w <= 2.0 * eps * hi) break;
+    if (w * r <= 1e-13 * ((hi + r) * (lo + r))) break;
+    const long long mb = (lb + hb) >> 1;
+    const double mid = __longlong_as_double(mb);
+    if (sturm_count(dd, e2, P, mid) > k) {
+      hi = mid;
+      hb = mb;
+    } else {
+      lo = mid;
+      lb = mb;
+    }
+  }
+  const double lam = 0.5 * (lo + hi) * inv_scale;
+  const double sc = __dmul_rn(beta, lam);
+  const double den = __dadd_rn(sc, alpha);
+  return den > 0.0 ? __ddiv_rn(sc, den) : 0.0;
+}
+
+}  // namespace bbml
