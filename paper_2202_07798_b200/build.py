@@ -32,6 +32,7 @@ def nvcc() -> str:
 def flags(verbose: bool = False) -> list[str]:
     f = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                 "-I", str(ROOT / "include"), "--expt-relaxed-constexpr"]
+    f += os.environ.get("BBML_NVCC_DEFS", "").split()  # development builds only
     if verbose:
         f += ["-Xptxas", "-v"]
     return f

@@ -17,6 +17,7 @@
 // upper triangle; LU + triangular solves and a parallel cyclic Jacobi
 // eigen-solver run in shared memory.
 #include <algorithm>
+#include <cstdio>
 #include <vector>
 
 #include "common.cuh"
@@ -858,12 +859,34 @@ __device__ double w_gamma_tri(WarpLm<PM>& S, int P, double alpha, double beta, i
   }
   __syncwarp();
   const double hi0 = (ghi + 2.220446049250313e-16 * tnorm) * scale;
-  const int n_neg = sturm_count(dd, e2, P, 0.0);
-  const double part = lane < P ? sturm_gamma_part(dd, e2, P, lane, n_neg, hi0, alpha / beta * scale,
-                                                  1.0 / scale, alpha, beta)
+  // pad T to PM rows (d = 2 > ||T||, e = 0) for the fixed-length Sturm loop
+  if (lane >= P && lane < PM) dd[lane] = 2.0;
+  if (lane + 1 >= P && lane < PM) e2[lane] = 0.0;
+  __syncwarp();
+  const int n_tiny = sturm_count_fixed<PM>(dd, e2, kSturmTiny);
+  const double part = lane < P ? sturm_gamma_part_fixed<PM>(dd, e2, lane, n_tiny, hi0,
+                                                            alpha / beta * scale, 1.0 / scale,
+                                                            alpha, beta)
                                : 0.0;
   return warp_sum(part);
 }
+
+
+// Development-only phase profiler (compile with -DBBML_LM_PROF, e.g.
+// BBML_NVCC_DEFS=-DBBML_LM_PROF python -m paper_2202_07798_b200.build):
+// lane 0 of every warp model accumulates clock64() per phase; totals are
+// printed to stderr after each bbml_lm_train call.
+#ifdef BBML_LM_PROF
+__device__ unsigned long long g_lm_prof[8];
+#define LM_PROF_T(v) long long v = clock64()
+#define LM_PROF_ADD(k, t0)                                                   \
+  do {                                                                       \
+    if (lane == 0) atomicAdd(&g_lm_prof[k], (unsigned long long)(clock64() - (t0))); \
+  } while (0)
+#else
+#define LM_PROF_T(v) (void)0
+#define LM_PROF_ADD(k, t0) (void)0
+#endif
 
 template <int PM, int D>
 __global__ void __launch_bounds__(128) lm_warp_kernel(LmLaunch L) {
@@ -914,20 +937,29 @@ __global__ void __launch_bounds__(128) lm_warp_kernel(LmLaunch L) {
   bool have_prev = false;
 
   for (int ep = 0; ep < tk.max_epochs; ++ep) {
-    if (!have_stats) w_stats<PM, D>(S, X, Y, n, d, h, P, xs, lane);
+    if (!have_stats) {
+      LM_PROF_T(t0);
+      w_stats<PM, D>(S, X, Y, n, d, h, P, xs, lane);
+      LM_PROF_ADD(0, t0);
+    }
     const double f0 = __dadd_rn(__dmul_rn(beta, e_d), __dmul_rn(alpha, e_w));
     bool accepted = false;
     double td = 0.0, tw = 0.0;
     while (true) {
       ++trials;
-      if (!w_solve<PM>(S, P, alpha, beta, mu, lane)) {
+      LM_PROF_T(t2);
+      const bool solved = w_solve<PM>(S, P, alpha, beta, mu, lane);
+      LM_PROF_ADD(2, t2);
+      if (!solved) {
         code = BBML_MODEL_SINGULAR;
         fail_mu = mu;
         break;
       }
       if (lane < P) S.wt[lane] = __dadd_rn(S.w[lane], S.delta[lane]);
       __syncwarp();
+      LM_PROF_T(t3);
       td = w_energy<PM, D>(S, S.wt, X, Y, n, d, h, xs, lane);
+      LM_PROF_ADD(3, t3);
       tw = 0.0;
       for (int i = 0; i < P; ++i) tw = fma(S.wt[i], S.wt[i], tw);
       const double f1 = __dadd_rn(__dmul_rn(beta, td), __dmul_rn(alpha, tw));
@@ -948,9 +980,13 @@ __global__ void __launch_bounds__(128) lm_warp_kernel(LmLaunch L) {
     double gamma = NAN;
     int pinned = 0;
     if (est) {
+      LM_PROF_T(t0);
       w_stats<PM, D>(S, X, Y, n, d, h, P, xs, lane);
+      LM_PROF_ADD(0, t0);
       have_stats = true;
+      LM_PROF_T(t1);
       gamma = PM > 8 ? w_gamma_tri<PM>(S, P, alpha, beta, lane) : w_gamma<PM>(S, P, alpha, beta, lane);
+      LM_PROF_ADD(1, t1);
       double na, nb;
       if (e_w > 0.0) {
         na = __ddiv_rn(gamma, __dmul_rn(2.0, e_w));
@@ -1130,6 +1166,17 @@ bbml_status lm_train_launch(const bbml_lm_task* tasks, int32_t n_tasks, const do
     if (e != cudaSuccess) return cuda_status(e, "lm_train launch");
   }
   if ((st = fork.join()) != BBML_OK) return st;
+#ifdef BBML_LM_PROF
+  {
+    unsigned long long pr[8];
+    cudaStreamSynchronize(stream);
+    cudaMemcpyFromSymbol(pr, g_lm_prof, sizeof(pr));
+    fprintf(stderr, "[lm_prof] Mcycles stats %.1f gamma %.1f solve %.1f energy %.1f\n", pr[0] * 1e-6,
+            pr[1] * 1e-6, pr[2] * 1e-6, pr[3] * 1e-6);
+    const unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_lm_prof, z, sizeof(z));
+  }
+#endif
   return scratch.release();
 }
 

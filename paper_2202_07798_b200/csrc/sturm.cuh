@@ -57,6 +57,74 @@ __device__ __forceinline__ int sturm_count(const double* __restrict__ dd,
   return cnt;
 }
 
+// Fixed-length variant for the warp path (P <= PM <= 32): T padded to PM
+// rows with d = 2 (> ||T||), e = 0, so the fully unrolled loop needs no
+// bounds and the padding never changes sign (dd/e2 in shared memory: the
+// broadcast loads are off the recurrence's dependency chain).  Pivot floor every row; the pair
+// is renormalised by its exponent every second row (the floor bounds the
+// per-row shrink by 2^-400, bisection points stay >= 2^-300, so two rows
+// cannot leave the normal range).
+template <int PM>
+__device__ __forceinline__ int sturm_count_fixed(const double* __restrict__ dd,
+                                                 const double* __restrict__ e2, double x) {
+  double p0 = 1.0, p1 = dd[0] - x;
+  p1 = fabs(p1) < kSturmPiv ? -kSturmPiv : p1;
+  int cnt = (int)((unsigned)__double2hiint(p1) >> 31);
+  auto row = [&](int j) {
+    const double fl = kSturmPiv * p1;
+    double p2 = fma(dd[j] - x, p1, -(e2[j - 1] * p0));
+    p2 = fabs(p2) < fabs(fl) ? -fl : p2;
+    cnt += (int)((unsigned)(__double2hiint(p2) ^ __double2hiint(p1)) >> 31);
+    p0 = p1;
+    p1 = p2;
+  };
+#pragma unroll 2
+  for (int j = 1; j < PM; j += 2) {
+    row(j);
+    if (j + 1 < PM) row(j + 1);
+    const int hm = max(__double2hiint(p0) & 0x7fffffff, __double2hiint(p1) & 0x7fffffff);
+    const double sc = __hiloint2double((2046 - (hm >> 20)) << 20, 0);
+    p0 *= sc;
+    p1 *= sc;
+  }
+  return cnt;
+}
+
+constexpr double kSturmTiny = 0x1p-300;  // scaled eigenvalues below this contribute 0
+
+// warp path: gamma contribution of the k-th smallest eigenvalue; n_tiny =
+// sturm_count_fixed(kSturmTiny) (eigenvalues below it, negative ones included,
+// are clipped to 0 -- their contribution is < 2^-300 / r)
+template <int PM>
+__device__ __forceinline__ double sturm_gamma_part_fixed(const double* __restrict__ dd,
+                                                         const double* __restrict__ e2, int k,
+                                                         int n_tiny,
+                                                       double hi0, double r, double inv_scale,
+                                                       double alpha, double beta) {
+  if (k < n_tiny || !(hi0 > kSturmTiny)) return 0.0;
+  double lo = kSturmTiny, hi = hi0;
+  long long lb = __double_as_longlong(lo), hb = __double_as_longlong(hi0);
+  constexpr double eps = 2.220446049250313e-16;
+  for (int it = 0; it < 80; ++it) {
+    const double w = hi - lo;
+    if (w <= 2.0 * eps * hi) break;
+    if (w * r <= 1e-13 * ((hi + r) * (lo + r))) break;
+    const long long mb = (lb + hb) >> 1;
+    const double mid = __longlong_as_double(mb);
+    if (sturm_count_fixed<PM>(dd, e2, mid) > k) {
+      hi = mid;
+      hb = mb;
+    } else {
+      lo = mid;
+      lb = mb;
+    }
+  }
+  const double lam = 0.5 * (lo + hi) * inv_scale;
+  const double sc = __dmul_rn(beta, lam);
+  const double den = __dadd_rn(sc, alpha);
+  return den > 0.0 ? __ddiv_rn(sc, den) : 0.0;
+}
+
 // gamma contribution of the k-th smallest eigenvalue (0-based).  dd/e2 are the
 // scaled diagonal and squared off-diagonal; hi0 = scaled Gershgorin upper
 // bound; n_neg = sturm_count(0); r = (alpha/beta) * scale; inv_scale = 1/scale.

@@ -11,7 +11,10 @@ R = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 series, spec, kw = bench.workload_series("suite16")
 so = lib()
 s = torch.cuda.current_stream()
+only = sys.argv[2].split(",") if len(sys.argv) > 2 else None
 for app in sorted({x.key[0] for x in series}):
+    if only and app not in only:
+        continue
     ss = [x for x in series if x.key[0] == app]
     kw2 = dict(kw); kw2["kinds"] = ("brbpnn",)
     wl = batch.build_workload(ss, spec, restarts=list(range(R)), precision=32, **kw2)
