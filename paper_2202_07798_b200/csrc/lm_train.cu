@@ -709,6 +709,85 @@ __device__ bool w_solve(WarpLm<PM>& S, int P, double alpha, double beta, double 
   return true;
 }
 
+// P <= 32 variant (h >= 2 models, parity gated statistically): same LU with
+// partial pivoting, but the trailing row update is unrolled over restrict
+// pointers (loads pipelined instead of serialised behind the stores) and both
+// substitutions are column-oriented (dtrsv order) with the right-hand side in
+// registers, one shuffle per column instead of a warp reduction per row.
+template <int PM>
+__device__ bool w_solve_cols(WarpLm<PM>& S, int P, double alpha, double beta, double mu, int lane) {
+  constexpr int LD = WarpLm<PM>::LD;
+  const double damp = __dadd_rn(mu, alpha);
+  if (lane < P) {
+    for (int b = 0; b < P; ++b) {
+      const double v = __dmul_rn(beta, S.jtj[lane * LD + b]);
+      S.A[lane * LD + b] = (lane == b) ? __dadd_rn(v, damp) : v;
+    }
+    S.rhs[lane] = -__dadd_rn(__dmul_rn(beta, S.jtr[lane]), __dmul_rn(alpha, S.w[lane]));
+  }
+  __syncwarp();
+  for (int k = 0; k < P; ++k) {
+    double best = (lane >= k && lane < P) ? fabs(S.A[lane * LD + k]) : -1.0;
+    int bi = lane;
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, m);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, m);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    const int p = bi;
+    if (S.A[p * LD + k] == 0.0) return false;
+    if (p != k) {
+      if (lane < P) {
+        const double t = S.A[k * LD + lane];
+        S.A[k * LD + lane] = S.A[p * LD + lane];
+        S.A[p * LD + lane] = t;
+      }
+      if (lane == 0) {
+        const double t = S.rhs[k];
+        S.rhs[k] = S.rhs[p];
+        S.rhs[p] = t;
+      }
+    }
+    __syncwarp();
+    if (lane > k && lane < P) {
+      double* __restrict__ ai = S.A + lane * LD;
+      const double* __restrict__ ak = S.A + k * LD;
+      const double l = __ddiv_rn(ai[k], ak[k]);
+      ai[k] = l;
+      int j = k + 1;
+      for (; j + 3 < P; j += 4) {
+        const double a0 = ai[j], a1 = ai[j + 1], a2 = ai[j + 2], a3 = ai[j + 3];
+        const double r0 = ak[j], r1 = ak[j + 1], r2 = ak[j + 2], r3 = ak[j + 3];
+        ai[j] = fma(-l, r0, a0);
+        ai[j + 1] = fma(-l, r1, a1);
+        ai[j + 2] = fma(-l, r2, a2);
+        ai[j + 3] = fma(-l, r3, a3);
+      }
+      for (; j < P; ++j) ai[j] = fma(-l, ak[j], ai[j]);
+    }
+    __syncwarp();
+  }
+  double r = lane < P ? S.rhs[lane] : 0.0;
+  for (int k = 0; k + 1 < P; ++k) {  // L y = Pb, unit lower, column by column
+    const double yk = __shfl_sync(0xffffffffu, r, k);
+    if (lane > k && lane < P) r = fma(-S.A[lane * LD + k], yk, r);
+  }
+  double mine = 0.0;
+  for (int i = P - 1; i >= 0; --i) {  // U x = y, column by column
+    double di = lane == i ? __ddiv_rn(r, S.A[i * LD + i]) : 0.0;
+    di = __shfl_sync(0xffffffffu, di, i);
+    if (lane == i) mine = di;
+    if (lane < i) r = fma(-S.A[lane * LD + i], di, r);
+  }
+  if (lane < P) S.delta[lane] = mine;
+  __syncwarp();
+  return true;
+}
+
 // gamma from the eigenvalues of J'J: cyclic Jacobi, round-robin disjoint
 // pairs, rotations skipped below max(eps * max|diag|, 1e-15 sqrt|a_pp a_qq|)
 // (LAPACK dsyevd's eigenvalues carry the same eps * ||A|| absolute accuracy)
@@ -816,17 +895,34 @@ __device__ double w_gamma_tri(WarpLm<PM>& S, int P, double alpha, double beta, i
     if (lane > k && lane < P) v[lane] = xi - (lane == k + 1 ? al : 0.0);
     __syncwarp();
     double pi = 0.0;
-    if (lane > k && lane < P) {
-      for (int j = k + 1; j < P; ++j) pi = fma(S.A[lane * LD + j], v[j], pi);
-      pi *= bh;
+    if (lane > k && lane < P) {  // four partial sums: the FMA chain is the latency
+      const double* __restrict__ ai = S.A + lane * LD;
+      double p1 = 0.0, p2 = 0.0, p3 = 0.0;
+      int j = k + 1;
+      for (; j + 3 < P; j += 4) {
+        pi = fma(ai[j], v[j], pi);
+        p1 = fma(ai[j + 1], v[j + 1], p1);
+        p2 = fma(ai[j + 2], v[j + 2], p2);
+        p3 = fma(ai[j + 3], v[j + 3], p3);
+      }
+      for (; j < P; ++j) pi = fma(ai[j], v[j], pi);
+      pi = ((pi + p1) + (p2 + p3)) * bh;
     }
     const double K = 0.5 * bh * warp_sum((lane > k && lane < P) ? v[lane] * pi : 0.0);
     if (lane > k && lane < P) wv[lane] = pi - K * v[lane];
     __syncwarp();
     if (lane > k && lane < P) {
+      double* __restrict__ ai = S.A + lane * LD;
       const double vi = v[lane], wi = wv[lane];
-      for (int j = k + 1; j < P; ++j)
-        S.A[lane * LD + j] -= fma(vi, wv[j], wi * v[j]);
+      int j = k + 1;
+      for (; j + 3 < P; j += 4) {
+        const double a0 = ai[j], a1 = ai[j + 1], a2 = ai[j + 2], a3 = ai[j + 3];
+        ai[j] = a0 - fma(vi, wv[j], wi * v[j]);
+        ai[j + 1] = a1 - fma(vi, wv[j + 1], wi * v[j + 1]);
+        ai[j + 2] = a2 - fma(vi, wv[j + 2], wi * v[j + 2]);
+        ai[j + 3] = a3 - fma(vi, wv[j + 3], wi * v[j + 3]);
+      }
+      for (; j < P; ++j) ai[j] -= fma(vi, wv[j], wi * v[j]);
     }
     if (lane == 0) ee[k] = al;
     __syncwarp();
@@ -948,7 +1044,8 @@ __global__ void __launch_bounds__(128) lm_warp_kernel(LmLaunch L) {
     while (true) {
       ++trials;
       LM_PROF_T(t2);
-      const bool solved = w_solve<PM>(S, P, alpha, beta, mu, lane);
+      const bool solved = PM > 8 ? w_solve_cols<PM>(S, P, alpha, beta, mu, lane)
+                                 : w_solve<PM>(S, P, alpha, beta, mu, lane);
       LM_PROF_ADD(2, t2);
       if (!solved) {
         code = BBML_MODEL_SINGULAR;

@@ -13,6 +13,7 @@
 //   gamma      : Householder tridiagonalisation + Sturm bisection (one or two
 //                eigenvalues per thread), like LAPACK dsytrd + dstebz
 #include <algorithm>
+#include <cstdio>
 #include <vector>
 
 #include "common.cuh"
@@ -21,6 +22,18 @@
 #include "pcg64.cuh"
 
 namespace bbml {
+
+#ifdef BBML_LM_PROF
+__device__ unsigned long long g_wide_prof[8];
+#define WP_T(v) long long v = clock64()
+#define WP_ADD(k, t0)                                                                     \
+  do {                                                                                    \
+    if (threadIdx.x == 0) atomicAdd(&g_wide_prof[k], (unsigned long long)(clock64() - (t0))); \
+  } while (0)
+#else
+#define WP_T(v) (void)0
+#define WP_ADD(k, t0) (void)0
+#endif
 
 constexpr int WNT = 256;
 constexpr int WWARPS = WNT / 32;
@@ -331,6 +344,7 @@ __device__ double wide_gamma(double* A, const double* jtj, int ld, int P, double
   for (int i = threadIdx.x; i < P; i += WNT) S.dd[i] = A[(int64_t)i * ld + i];
   if (threadIdx.x == 0 && P >= 2) S.ee[P - 2] = A[(int64_t)(P - 1) * ld + (P - 2)];
   __syncthreads();
+  WP_T(tb);
   double glo = 1e308, ghi = -1e308;
   for (int i = threadIdx.x; i < P; i += WNT) {
     const double r = (i > 0 ? fabs(S.ee[i - 1]) : 0.0) + (i + 1 < P ? fabs(S.ee[i]) : 0.0);
@@ -357,7 +371,9 @@ __device__ double wide_gamma(double* A, const double* jtj, int ld, int P, double
   double part = 0.0;
   for (int idx = threadIdx.x; idx < P; idx += WNT)
     part += sturm_gamma_part(S.dd, S.e2, P, idx, n_neg, hi0, r, 1.0 / scale, alpha, beta);
-  return bsum(part, S);
+  const double g = bsum(part, S);
+  WP_ADD(4, tb);
+  return g;
 }
 
 __global__ void __launch_bounds__(WNT) lm_wide_kernel(WideLaunch L) {
@@ -399,20 +415,29 @@ __global__ void __launch_bounds__(WNT) lm_wide_kernel(WideLaunch L) {
   bool have_prev = false;
 
   for (int ep = 0; ep < tk.max_epochs; ++ep) {
-    if (!have_stats) wide_stats(J, R, jtj, ld, X, Y, n, d, h, P, xs, S);
+    if (!have_stats) {
+      WP_T(t0);
+      wide_stats(J, R, jtj, ld, X, Y, n, d, h, P, xs, S);
+      WP_ADD(0, t0);
+    }
     const double f0 = __dadd_rn(__dmul_rn(beta, e_d), __dmul_rn(alpha, e_w));
     bool accepted = false;
     double td = 0.0, tw = 0.0;
     while (true) {
       ++trials;
-      if (!wide_solve(A, jtj, ld, P, alpha, beta, mu, S)) {
+      WP_T(t2);
+      const bool solved = wide_solve(A, jtj, ld, P, alpha, beta, mu, S);
+      WP_ADD(2, t2);
+      if (!solved) {
         code = BBML_MODEL_SINGULAR;
         fail_mu = mu;
         break;
       }
       for (int i = threadIdx.x; i < P; i += WNT) S.wt[i] = __dadd_rn(S.w[i], S.delta[i]);
       __syncthreads();
+      WP_T(t3);
       td = wide_energy(S.wt, X, Y, n, d, h, xs, S);
+      WP_ADD(3, t3);
       tw = 0.0;
       for (int i = 0; i < P; ++i) tw = fma(S.wt[i], S.wt[i], tw);
       const double f1 = __dadd_rn(__dmul_rn(beta, td), __dmul_rn(alpha, tw));
@@ -434,9 +459,13 @@ __global__ void __launch_bounds__(WNT) lm_wide_kernel(WideLaunch L) {
     double gamma = NAN;
     int pinned = 0;
     if (est) {
+      WP_T(t0);
       wide_stats(J, R, jtj, ld, X, Y, n, d, h, P, xs, S);
+      WP_ADD(0, t0);
       have_stats = true;
+      WP_T(t1);
       gamma = wide_gamma(A, jtj, ld, P, alpha, beta, S);
+      WP_ADD(1, t1);
       double na, nb;
       if (e_w > 0.0) {
         na = __ddiv_rn(gamma, __dmul_rn(2.0, e_w));
@@ -529,6 +558,17 @@ bbml_status lm_wide_launch(const bbml_lm_task* d_tasks, const int32_t* d_orig,
   L.ld = ld;
   lm_wide_kernel<<<n_tasks, WNT, 0, s>>>(L);
   cudaError_t e = cudaGetLastError();
+#ifdef BBML_LM_PROF
+  {
+    unsigned long long pr[8];
+    cudaStreamSynchronize(s);
+    cudaMemcpyFromSymbol(pr, g_wide_prof, sizeof(pr));
+    fprintf(stderr, "[wide_prof] Mcycles stats %.1f gamma %.1f (bisect %.1f) solve %.1f energy %.1f\n",
+            pr[0] * 1e-6, pr[1] * 1e-6, pr[4] * 1e-6, pr[2] * 1e-6, pr[3] * 1e-6);
+    const unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_wide_prof, z, sizeof(z));
+  }
+#endif
   return e == cudaSuccess ? BBML_OK : cuda_status(e, "lm_wide launch");
 }
 
