@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(LM_NT) lm_train_kernel(LmLaunch L) {
 // __syncwarp only.
 // ===========================================================================
 template <int PM>
-struct WarpLm {
+struct alignas(16) WarpLm {
   static constexpr int LD = PM + 1;
   static constexpr int NE = PM * (PM + 1) / 2 + PM;
   double w[PM], wt[PM], delta[PM], jtr[PM], rhs[PM];
@@ -562,6 +562,94 @@ __device__ double w_energy(const WarpLm<PM>& S, const double* wv, const double* 
   return warp_sum(acc);
 }
 
+// P <= 32 statistics (generic h, d): rows of [J | r] are staged CH at a time
+// in the LU workspace (idle during the statistics), one sample per lane, then
+// each lane accumulates 4x4 register blocks of the upper triangle of
+// [J r]'[J r] (45 blocks over 9 column blocks, two per lane) in sample order
+// -- the same order and rounding as the per-entry loop, with 8x fewer shared
+// loads per FMA.
+template <int PM>
+__device__ void w_stats_blocked(WarpLm<PM>& S, const double* X, const double* Y, int n, int d,
+                                int h, int P, int xs, int lane) {
+  constexpr int LD = WarpLm<PM>::LD;
+  constexpr int RW = 36;               // J columns (P <= 32) + r, padded to 9 blocks of 4
+  constexpr int CH = (PM * LD) / RW;   // staged rows per chunk (29 at PM = 32)
+  constexpr int NB = RW / 4;
+  constexpr int NBLK = NB * (NB + 1) / 2;
+  static_assert(NBLK <= 64, "two blocks per lane");
+  double* Jc = S.A;
+  int ba[2], bb[2];
+  bool valid[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    int t = lane + 32 * u, r = 0;
+    valid[u] = t < NBLK;
+    if (!valid[u]) t = 0;
+    while (t >= NB - r) {
+      t -= NB - r;
+      ++r;
+    }
+    ba[u] = r;
+    bb[u] = r + t;
+  }
+  double acc[2][4][4];
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[u][p][q] = 0.0;
+  double x[BBML_MAX_INPUTS];
+  for (int base = 0; base < n; base += CH) {
+    const int cnt = min(CH, n - base);
+    __syncwarp();
+    if (lane < cnt) {
+      const int i = base + lane;
+      for (int k = 0; k < d; ++k) x[k] = __ldg(X + (int64_t)i * xs + k);
+      double* row = Jc + lane * RW;
+      row[P] = __dsub_rn(br_sample(S.w, x, d, h, row), __ldg(Y + i));
+      for (int c = P + 1; c < RW; ++c) row[c] = 0.0;
+    }
+    __syncwarp();
+    for (int c = 0; c < cnt; ++c) {
+      const double* row = Jc + c * RW;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!valid[u]) continue;
+        const double2 a01 = *(const double2*)(row + 4 * ba[u]);
+        const double2 a23 = *(const double2*)(row + 4 * ba[u] + 2);
+        const double2 b01 = *(const double2*)(row + 4 * bb[u]);
+        const double2 b23 = *(const double2*)(row + 4 * bb[u] + 2);
+        const double va[4] = {a01.x, a01.y, a23.x, a23.y};
+        const double vb[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[u][p][q] = fma(va[p], vb[q], acc[u][p][q]);
+      }
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    if (!valid[u]) continue;
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int a = 4 * ba[u] + p, b = 4 * bb[u] + q;
+        if (a > b || a >= P) continue;
+        if (b < P) {
+          S.jtj[a * LD + b] = acc[u][p][q];
+          S.jtj[b * LD + a] = acc[u][p][q];
+        } else if (b == P) {
+          S.jtr[a] = acc[u][p][q];
+        }
+      }
+  }
+  __syncwarp();
+}
+
 template <int PM, int D>
 __device__ void w_stats(WarpLm<PM>& S, const double* X, const double* Y, int n, int d, int h, int P,
                         int xs, int lane) {
@@ -610,6 +698,8 @@ __device__ void w_stats(WarpLm<PM>& S, const double* X, const double* Y, int n, 
       const double v = warp_sum(acc[e]);
       if (lane == 0) S.jtr[p] = v;
     }
+  } else if constexpr (PM > 8) {
+    w_stats_blocked<PM>(S, X, Y, n, d, h, P, xs, lane);
   } else {
     const int ne = P * (P + 1) / 2 + P;
     double x[BBML_MAX_INPUTS];
