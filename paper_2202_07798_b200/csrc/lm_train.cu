@@ -479,13 +479,17 @@ struct alignas(16) WarpLm {
   double w[PM], wt[PM], delta[PM], jtr[PM], rhs[PM];
   double jtj[PM * LD];
   double A[PM * LD];
-  static constexpr int JCH = PM > 8 ? 8 : 32;  // staged Jacobian rows per chunk
+  // PM = 32 (statistics staged in A, Householder + bisection gamma) only needs
+  // the tridiagonal (dd, e2, ee) here; the per-entry statistics tables and the
+  // Jacobi schedule exist for PM = 8 only (smaller footprint -> more warps/SM)
+  static constexpr bool kWide = PM > 8;
+  static constexpr int JCH = kWide ? 3 : 32;  // staged Jacobian rows per chunk (PM = 8)
   double Jc[JCH * PM];
-  double rc[JCH];
-  double cs[2 * 16];
-  int pq[16];
-  unsigned short ent[NE];  // (a << 8 | b) for the upper triangle, b == P -> J'r
-  unsigned short rr[(PM > 1 ? PM - 1 : 1) * (PM / 2)];  // round-robin pair schedule (p | q << 8)
+  double rc[kWide ? 2 : JCH];
+  double cs[kWide ? 2 : 2 * 16];
+  int pq[kWide ? 2 : 16];
+  unsigned short ent[kWide ? 4 : NE];  // (a << 8 | b) for the upper triangle, b == P -> J'r
+  unsigned short rr[kWide ? 4 : (PM - 1) * (PM / 2)];  // round-robin pair schedule (p | q << 8)
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -1097,16 +1101,18 @@ __global__ void __launch_bounds__(128) lm_warp_kernel(LmLaunch L) {
     const int hd = h * d;
     for (int i = 0; i < hd + h; ++i) S.w[i] = rng.uniform(-s1, s1);
     for (int i = hd + h; i < P; ++i) S.w[i] = rng.uniform(-s2, s2);
-    int e = 0;  // upper-triangle entry table for the generic stats path
-    for (int a = 0; a < P; ++a)
-      for (int b = a; b <= P; ++b) S.ent[e++] = (unsigned short)((a << 8) | b);
-    const int Pp = (P + 1) & ~1;  // Jacobi round-robin schedule (index P = bye when P is odd)
-    for (int r = 0; r < Pp - 1; ++r)
-      for (int k = 0; k < Pp / 2; ++k) {
-        const int pa = k == 0 ? 0 : 1 + ((k - 1 + r) % (Pp - 1));
-        const int qa = 1 + ((Pp - 2 - k + r) % (Pp - 1));
-        S.rr[r * (PM / 2) + k] = (unsigned short)(min(pa, qa) | (max(pa, qa) << 8));
-      }
+    if constexpr (!WarpLm<PM>::kWide) {
+      int e = 0;  // upper-triangle entry table for the generic stats path
+      for (int a = 0; a < P; ++a)
+        for (int b = a; b <= P; ++b) S.ent[e++] = (unsigned short)((a << 8) | b);
+      const int Pp = (P + 1) & ~1;  // Jacobi round-robin schedule (index P = bye when P is odd)
+      for (int r = 0; r < Pp - 1; ++r)
+        for (int k = 0; k < Pp / 2; ++k) {
+          const int pa = k == 0 ? 0 : 1 + ((k - 1 + r) % (Pp - 1));
+          const int qa = 1 + ((Pp - 2 - k + r) % (Pp - 1));
+          S.rr[r * (PM / 2) + k] = (unsigned short)(min(pa, qa) | (max(pa, qa) << 8));
+        }
+    }
   }
   __syncwarp();
 
@@ -1172,7 +1178,8 @@ __global__ void __launch_bounds__(128) lm_warp_kernel(LmLaunch L) {
       LM_PROF_ADD(0, t0);
       have_stats = true;
       LM_PROF_T(t1);
-      gamma = PM > 8 ? w_gamma_tri<PM>(S, P, alpha, beta, lane) : w_gamma<PM>(S, P, alpha, beta, lane);
+      if constexpr (WarpLm<PM>::kWide) gamma = w_gamma_tri<PM>(S, P, alpha, beta, lane);
+      else gamma = w_gamma<PM>(S, P, alpha, beta, lane);
       LM_PROF_ADD(1, t1);
       double na, nb;
       if (e_w > 0.0) {
@@ -1236,7 +1243,7 @@ __global__ void __launch_bounds__(128) lm_warp_kernel(LmLaunch L) {
 
 template <int PM, int D>
 static cudaError_t lm_launch_warp(const LmLaunch& L, cudaStream_t s) {
-  const int warps = PM > 8 ? 2 : 4;  // PM = 32: ~23 KB smem per warp -> 2-warp CTAs pack 10 per SM
+  const int warps = PM > 8 ? 3 : 4;  // PM = 32: 19 KB smem per warp -> 3-warp CTAs pack 12 warps per SM
   const size_t smem = warps * sizeof(WarpLm<PM>);
   auto k = lm_warp_kernel<PM, D>;
   if (smem > 48 * 1024) {
