@@ -47,7 +47,15 @@ def parse():
     return ap.parse_args()
 
 
-DEFAULT_RESTARTS = {"suite16": 32, "app20": 1, "sweep": 16, "wide": 1}
+# restarts per GPU: suite16 32 (fills the GPU), sweep 16 (SURVEY §8d cfg 4), wide 7
+# (140 CTA-per-model BR-BPNN fits on 148 SMs)
+DEFAULT_RESTARTS = {"suite16": 32, "app20": 1, "sweep": 16, "wide": 7}
+
+# BR-BPNN tasks at or above this hidden size are timed on the CPU for
+# CPU_EPOCH_SAMPLE epochs and extrapolated per epoch (a full h = 64 fit takes
+# minutes of CPU time); SURVEY §8d "time a sample and extrapolate"
+CPU_WIDE_HIDDEN = 32
+CPU_EPOCH_SAMPLE = 3
 
 
 def workload_series(name: str):
@@ -151,16 +159,23 @@ def measure_fma_peak(torch, precision):
 # ---------------------------------------------------------------------------
 
 def _cpu_task(args):
+    """Seconds for one model on one core; wide BR fits are timed for
+    CPU_EPOCH_SAMPLE epochs and scaled to `full_epochs` epochs."""
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     from oracle import bbml_oracle as O
 
-    key, X, y, kind, mode, frac, base, br_hidden = args
+    key, X, y, kind, mode, frac, base, br_hidden, full_epochs = args
+    sampled = kind == "brbpnn" and br_hidden >= CPU_WIDE_HIDDEN
     t0 = time.perf_counter()
-    O.train_one(key, X, y, kind, mode=mode, fraction=frac, base_seed=base, br_hidden=br_hidden)
-    return time.perf_counter() - t0
+    r = O.train_one(key, X, y, kind, mode=mode, fraction=frac, base_seed=base, br_hidden=br_hidden,
+                    br_max_epochs=CPU_EPOCH_SAMPLE if sampled else 1000)
+    dt = time.perf_counter() - t0
+    if sampled and r.epochs_run:
+        dt *= full_epochs / r.epochs_run
+    return dt
 
 
-def cpu_sample_tasks(series, spec, wl_kw, restarts, sample):
+def cpu_sample_tasks(series, spec, wl_kw, restarts, sample, full_epochs=1000):
     """Stratified sample: tasks ordered by a cost estimate, one pick per
     equal-count stratum (median of the stratum)."""
     kinds = wl_kw.get("kinds", ("pnn", "brbpnn"))
@@ -175,22 +190,25 @@ def cpu_sample_tasks(series, spec, wl_kw, restarts, sample):
     tasks.sort(key=lambda t: t[0])
     S = min(sample, len(tasks))
     picks = [tasks[int((i + 0.5) * len(tasks) / S)] for i in range(S)]
-    return [(s.key, s.X, s.y, kind, spec.mode.value, spec.fraction, r % max(restarts, 1), h)
-            for i, (_, s, kind, h) in enumerate(picks) for r in (i,)]
+    return [(s.key, s.X, s.y, kind, spec.mode.value, spec.fraction, r % max(restarts, 1), h,
+             full_epochs) for i, (_, s, kind, h) in enumerate(picks) for r in (i,)]
 
 
-def run_cpu(series, spec, wl_kw, restarts, sample, cores):
+def run_cpu(series, spec, wl_kw, restarts, sample, cores, full_epochs=1000):
     from concurrent.futures import ProcessPoolExecutor
 
-    jobs = cpu_sample_tasks(series, spec, wl_kw, restarts, sample)
+    jobs = cpu_sample_tasks(series, spec, wl_kw, restarts, sample, full_epochs)
     t0 = time.perf_counter()
     with ProcessPoolExecutor(max_workers=cores) as pool:
         secs = list(pool.map(_cpu_task, jobs, chunksize=1))
     wall = time.perf_counter() - t0
     # ideal-pool throughput: every core busy, mean per-model time of the
     # stratified sample (favourable to the CPU: ignores the straggler tail)
+    wide = any(j[3] == "brbpnn" and j[7] >= CPU_WIDE_HIDDEN for j in jobs)
     return {"models_per_s": cores * len(jobs) / sum(secs), "wall_s": wall, "n": len(jobs),
-            "mean_model_s": sum(secs) / len(jobs)}
+            "mean_model_s": sum(secs) / len(jobs),
+            "note": (f"; BR-BPNN h>={CPU_WIDE_HIDDEN} fits timed for {CPU_EPOCH_SAMPLE} epochs and "
+                     f"scaled to {full_epochs:.0f} epochs" if wide else "")}
 
 
 def reference_arm(args, world, rank):
@@ -216,7 +234,8 @@ def reference_arm(args, world, rank):
                          "sample": f"{vals[0]['n']} stratified tasks/step (one median pick per "
                                    f"equal-count cost stratum) of the {args.workload} workload; "
                                    "ideal-pool throughput = cores / mean per-model seconds; "
-                                   "oracle/bbml_oracle.py (bit-identical to the reference)"},
+                                   "oracle/bbml_oracle.py (bit-identical to the reference)"
+                                   + vals[0]["note"]},
         "e2e": {"value": v, "unit": "models/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -349,7 +368,10 @@ def main():
                          "kernel_ms": pnn_ms, "algorithmic_flops": pnn_fl, "traffic": None}
         if lm_ms:
             a = lm_fl / (lm_ms * 1e-3) / 1e12
-            rl["lm"] = {"bound": "fp64-pipe", "kernel": "lm_warp_kernel (bbml_lm_train)",
+            Pl = wl.lm["h"] * (wl.lm["d"] + 2) + 1
+            kn = " + ".join(k for k, m in (("lm_warp_kernel", (Pl <= 32).any()),
+                                           ("lm_wide_kernel", (Pl > 32).any())) if m)
+            rl["lm"] = {"bound": "fp64-pipe", "kernel": f"{kn} (bbml_lm_train)",
                         "achieved": a, "peak": peak64, "unit": "TFLOP/s", "frac": a / peak64,
                         "kernel_ms": lm_ms, "algorithmic_flops": lm_fl, "traffic": None}
         dom = max(rl, key=lambda k: rl[k]["kernel_ms"]) if rl else None
@@ -360,11 +382,15 @@ def main():
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
-            r = run_cpu(series, spec, kw, restarts, args.cpu_sample or max(32, 4 * cores), cores)
+            wide_ep = (float(st_lm["epochs"][wl.lm["h"] >= CPU_WIDE_HIDDEN].mean())
+                       if len(wl.lm) and (wl.lm["h"] >= CPU_WIDE_HIDDEN).any() else 1000.0)
+            r = run_cpu(series, spec, kw, restarts, args.cpu_sample or max(32, 4 * cores), cores,
+                        wide_ep)
             cpu = {"value": r["models_per_s"], "unit": "models/s", "cores": cores, "kind": "port",
                    "sample": f"{r['n']} stratified tasks (median pick per equal-count cost stratum) "
                              f"of {args.workload}; ideal-pool throughput = cores / mean per-model "
-                             f"seconds ({r['mean_model_s']:.3f} s); wall {r['wall_s']:.1f} s"}
+                             f"seconds ({r['mean_model_s']:.3f} s); wall {r['wall_s']:.1f} s"
+                             + r["note"]}
         line = {
             "metric": "models trained/sec", "value": value, "unit": "models/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -381,6 +407,11 @@ def main():
             "roofline": roof,
             "gpu_launches": launches,
             "models_failed": n_bad,
+            "workload_stats": {
+                "lm_epochs_mean": float(st_lm["epochs"].mean()) if len(wl.lm) else None,
+                "lm_trials_mean": float(st_lm["trials"].mean()) if len(wl.lm) else None,
+                "pnn_max_sequential_steps": int((wl.pnn["epochs"] * -(-wl.pnn["n"] // wl.pnn["batch"])).max())
+                if len(wl.pnn) else None},
             "clocks": summarize_clocks(clock_path, local),
             "cpu_baseline": cpu,
             "step_ms": step_ms,

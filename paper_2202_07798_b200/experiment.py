@@ -166,6 +166,9 @@ def train_many(pairs: Sequence[tuple], config: ExperimentConfig, *, precision: O
                br_hidden_of=None, prepared: Optional[dict] = None) -> BatchOutput:
     """Train and evaluate every (series, kind) pair with batched kernels.
 
+    A pair may carry its own split as a third element, ``(series, kind,
+    SplitSpec)`` (learning curves: one split per training fraction, all in
+    the same launch); otherwise ``config.split_spec()`` applies.
     ``br_hidden_of(series) -> int`` optionally overrides ``config.br_hidden``
     per series (e.g. hidden 10 for gramschmit).
     Returns SeriesResult objects in input order, identical in meaning to
@@ -178,13 +181,16 @@ def train_many(pairs: Sequence[tuple], config: ExperimentConfig, *, precision: O
     results: list = [None] * len(pairs)
     tasks: dict = {"pnn": [], "brbpnn": []}
     order: dict = {"pnn": [], "brbpnn": []}
-    for i, (series, kind) in enumerate(pairs):
+    for i, pair in enumerate(pairs):
+        series, kind = pair[0], pair[1]
+        sp = pair[2] if len(pair) > 2 else spec
         res = SeriesResult(series.key, kind)
         results[i] = res
-        p = cache.get(id(series))
+        ck = id(series) if sp is spec else (id(series), sp.mode, sp.fraction, sp.seed)
+        p = cache.get(ck)
         if p is None:
-            p = prepare(series, spec)
-            cache[id(series)] = p
+            p = prepare(series, sp)
+            cache[ck] = p
         if p.error is not None:
             res.error = p.error
             continue
@@ -337,23 +343,55 @@ class CurvePoint:
     skipped: bool = False
 
 
+def learning_curves(series_list: Sequence[BbSeries], kinds: Sequence[str],
+                    fractions: Sequence[float], seed: int,
+                    config: Optional[ExperimentConfig] = None, *, br_hidden_of=None) -> dict:
+    """Batched learning curves (the reference's ``cmd_sweep``
+    loop, cli.py:232-237, over ``learning_curve``, experiment.py:221-253):
+    every (series, kind, fraction) fit of the sweep is one task of ONE
+    ``train_many`` call -- a PNN launch and an LM launch for the whole sweep.
+    Returns ``{(series.key, kind): [CurvePoint per fraction]}``; points are
+    identical in meaning to calling ``learning_curve`` per series and kind
+    (random split at each fraction under the shared seed; degenerate splits
+    and failed fits are skipped, not fatal)."""
+    config = ExperimentConfig() if config is None else config
+    cfg = ExperimentConfig(**{**config.__dict__, "split_mode": SplitMode.RANDOM, "seed": seed})
+    specs = [SplitSpec(SplitMode.RANDOM, float(f), seed) for f in fractions]
+    triples = [(s, k, sp) for s in series_list for k in kinds for sp in specs]
+    out = train_many(triples, cfg, br_hidden_of=br_hidden_of).results if triples else []
+    curves: dict = {}
+    for (s, k, sp), r in zip(triples, out):
+        pt = (CurvePoint(sp.fraction, None, skipped=True) if r.error is not None
+              else CurvePoint(sp.fraction, r.accuracy))
+        curves.setdefault((s.key, k), []).append(pt)
+    return curves
+
+
 def learning_curve(series: BbSeries, kind: str, fractions: Sequence[float], seed: int,
                    config: Optional[ExperimentConfig] = None) -> list:
-    """Random-split accuracy per training fraction (experiment.py:221-253);
-    every fraction is one task of a single batched device call per fraction."""
-    config = ExperimentConfig() if config is None else config
-    pts = []
-    for f in fractions:
-        cfg = ExperimentConfig(**{**config.__dict__, "split_mode": SplitMode.RANDOM,
-                                  "fraction": f, "seed": seed})
-        try:
-            r = train_one(series, kind, cfg)
-        except SplitError:
-            pts.append(CurvePoint(f, None, skipped=True))
-            continue
-        pts.append(CurvePoint(f, None, skipped=True) if r.error is not None
-                   else CurvePoint(f, r.accuracy))
-    return pts
+    """Random-split accuracy per training fraction (experiment.py:221-253),
+    all fractions in one batched device call."""
+    return learning_curves([series], [kind], fractions, seed, config)[(series.key, kind)]
+
+
+def run_sweep(series_list: Sequence[BbSeries], config: ExperimentConfig, out_dir,
+              fractions: Sequence[float], seed: int, input_digests=None) -> int:
+    """``bbcount sweep`` (cli.py:217-248) minus argument parsing: every curve of
+    the sweep from one batched call, written as ``curve_<slug>.csv`` plus
+    ``sweep_manifest.json``.  Returns the number of curves."""
+    out_dir = Path(out_dir)
+    out_dir.mkdir(parents=True, exist_ok=True)
+    fractions = sorted(float(f) for f in fractions)
+    curves = learning_curves(series_list, config.models, fractions, seed, config)
+    for s in series_list:
+        for kind in config.models:
+            write_curve_csv(curves[(s.key, kind)], out_dir / f"curve_{series_slug(s.key, kind)}.csv")
+    manifest = {"config": config.to_manifest(), "fractions": fractions,
+                "inputs": dict(input_digests or {}), "curves": len(curves)}
+    with open(out_dir / "sweep_manifest.json", "w", encoding="utf-8", newline="\n") as fh:
+        json.dump(manifest, fh, indent=2)
+        fh.write("\n")
+    return len(curves)
 
 
 # ---------------------------------------------------------------------------

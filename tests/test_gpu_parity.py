@@ -254,3 +254,49 @@ def test_train_one_matches_reference_golden(golden):
             assert _rel(got, g[p + "counts_q"], floor) <= tol, (key, kind)
             checked += 1
     assert checked >= 60
+
+
+def test_learning_curves_batched_match_oracle(tmp_path):
+    """a whole learning-curve sweep (series x kinds x
+    fractions) in one batched call.  Every point equals the single-task
+    device result bit for bit (models are independent), matches the oracle's
+    train_one on the same random split (PNN FP64 / BR hidden 1: accuracy
+    within 1e-6 pp), and skipped points (degenerate splits) agree."""
+    import json
+
+    from paper_2202_07798_b200 import synth
+    from paper_2202_07798_b200.experiment import (ExperimentConfig, learning_curves, run_sweep,
+                                                   train_one)
+    from paper_2202_07798_b200.metrics import accuracy_percent
+    from paper_2202_07798_b200.traces import BbSeries, SplitMode
+
+    raw = synth.app20()[:3]
+    series = [BbSeries(k, X, y) for k, X, y in raw]
+    fr = (0.02, 0.1, 0.3, 0.5, 0.7, 0.9)
+    seed = 5
+    cfg = ExperimentConfig(pnn_epochs=40, br_max_epochs=60)
+    curves = learning_curves(series, ("pnn", "brbpnn"), fr, seed, cfg)
+    assert len(curves) == 6
+    n_pts = 0
+    for s in series:
+        for kind in ("pnn", "brbpnn"):
+            pts = curves[(s.key, kind)]
+            assert [p.fraction for p in pts] == list(fr)
+            for p in pts:
+                o = O.train_one(s.key, s.X, s.y, kind, mode="random", fraction=p.fraction,
+                                base_seed=seed, pnn_epochs=40, br_max_epochs=60)
+                if o.error is not None:
+                    assert p.skipped, (s.key, kind, p.fraction, o.error)
+                    continue
+                assert not p.skipped, (s.key, kind, p.fraction)
+                assert abs(p.accuracy - accuracy_percent(o.mse)) <= 1e-6, (s.key, kind, p.fraction)
+                n_pts += 1
+            single = train_one(s, kind, ExperimentConfig(**{**cfg.__dict__, "split_mode": SplitMode.RANDOM,
+                                                            "fraction": 0.7, "seed": seed}))
+            assert single.accuracy == pts[fr.index(0.7)].accuracy
+    assert n_pts >= 24
+    n = run_sweep(series, cfg, tmp_path, fr, seed)
+    assert n == 6
+    man = json.loads((tmp_path / "sweep_manifest.json").read_text())
+    assert man["curves"] == 6 and man["fractions"] == sorted(fr)
+    assert len(list(tmp_path.glob("curve_*.csv"))) == 6
