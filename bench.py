@@ -194,12 +194,21 @@ def cpu_sample_tasks(series, spec, wl_kw, restarts, sample, full_epochs=1000):
              full_epochs) for i, (_, s, kind, h) in enumerate(picks) for r in (i,)]
 
 
+def _cpu_worker_init():
+    # one BLAS thread per worker process: the pool provides the parallelism
+    # (numpy is already imported in the parent, so the env var alone is too late)
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from threadpoolctl import threadpool_limits
+
+    threadpool_limits(1)
+
+
 def run_cpu(series, spec, wl_kw, restarts, sample, cores, full_epochs=1000):
     from concurrent.futures import ProcessPoolExecutor
 
     jobs = cpu_sample_tasks(series, spec, wl_kw, restarts, sample, full_epochs)
     t0 = time.perf_counter()
-    with ProcessPoolExecutor(max_workers=cores) as pool:
+    with ProcessPoolExecutor(max_workers=cores, initializer=_cpu_worker_init) as pool:
         secs = list(pool.map(_cpu_task, jobs, chunksize=1))
     wall = time.perf_counter() - t0
     # ideal-pool throughput: every core busy, mean per-model time of the
