@@ -2,14 +2,16 @@
 // (33 <= P <= 512, e.g. hidden 64 at d = 2 -> P = 257; BASELINE config 5).
 //
 // Same semantics as lm_train.cu (brbpnn.py:286-346, see there for line refs),
-// one model per CTA of 256 threads.  The P x P matrices (J'J and the LU /
-// tridiagonalisation workspace) and the n x P Jacobian live in a per-model
-// global scratch slab that stays L2-resident (126 MB L2); vectors live in
-// shared memory.
-//   J'J        : 4x4 register tiles over the upper triangle, streamed over the
-//                n Jacobian rows (J written once per pass by the row kernel)
-//   solve      : right-looking LU with partial pivoting (dgetf2 order), block
-//                argmax, triangular solves with block reductions
+// one model per CTA of 256 threads.  The P x P matrices (J'J and the
+// factorisation / tridiagonalisation workspace) live in a per-model global
+// scratch slab (L2-resident for ~100 models); vectors, the staged [J r] rows
+// and the Cholesky panel live in shared memory.  No Jacobian is materialised.
+//   J'J, J'r   : [J r] rows generated 32 at a time into shared memory, 4x4
+//                register blocks of the upper triangle (wide_stats_chunked)
+//   solve      : blocked Cholesky (32-column panels, panel in shared memory,
+//                register-blocked trailing update) + blocked substitutions;
+//                LU with partial pivoting (dgetf2 order) if a pivot is not
+//                positive (wide_chol / wide_solve)
 //   gamma      : Householder tridiagonalisation + Sturm bisection (one or two
 //                eigenvalues per thread), like LAPACK dsytrd + dstebz
 #include <algorithm>
@@ -119,56 +121,295 @@ __device__ double wide_energy(const double* wv, const double* X, const double* Y
   return bsum(acc, S);
 }
 
-// J (n x ldj) rows + residuals, then J'J (upper 4x4 tiles, mirrored) and J'r
-__device__ void wide_stats(double* J, double* R, double* jtj, int ld, const double* X, const double* Y,
-                           int n, int d, int h, int P, int xs, WideSmem& S) {
-  double x[BBML_MAX_INPUTS];
-  for (int i = threadIdx.x; i < n; i += WNT) {
-    for (int k = 0; k < d; ++k) x[k] = __ldg(X + (int64_t)i * xs + k);
-    double* jr = J + (int64_t)i * ld;
-    R[i] = __dsub_rn(wide_sample(S.w, x, d, h, jr), __ldg(Y + i));
-    for (int c = P; c < ld; ++c) jr[c] = 0.0;
-  }
-  __syncthreads();
-  const int nt = ld / 4;
-  const int ntiles = nt * (nt + 1) / 2;
-  for (int t = threadIdx.x; t < ntiles; t += WNT) {
-    int ta = 0, rem = t;  // t -> (ta <= tb) row-major upper triangle of tiles
-    while (rem >= nt - ta) {
-      rem -= nt - ta;
-      ++ta;
+// J'J and J'r without a Jacobian slab: rows of [J | r] are generated 32 at a
+// time into shared memory (one (row, hidden unit) item per thread, then the
+// residual per row in the reference's summation order) and every thread
+// accumulates 4x4 register blocks of the upper triangle of [J r]'[J r] over
+// all rows (sample order: the same order and rounding as the per-entry sum).
+// Three register blocks per thread per pass; passes regenerate the chunk.
+constexpr int WCH = 32;  // staged rows per chunk
+constexpr int WRB = 3;   // 4x4 blocks per thread per pass
+
+__device__ __forceinline__ int wide_rw(int P) { return (P + 1 + 3) & ~3; }
+
+__device__ void wide_stats_chunked(double* jtj, int ld, const double* X, const double* Y, int n, int d,
+                                   int h, int P, int xs, WideSmem& S, double* Jc) {
+  const int rw = wide_rw(P);  // row width: P J columns, r, zero pad
+  const int nbk = rw / 4;
+  const int ntiles = nbk * (nbk + 1) / 2;
+  const int hd = h * d;
+  const int per_pass = WNT * WRB;
+  for (int t0 = 0; t0 < ntiles; t0 += per_pass) {
+    int ta[WRB], tb[WRB];
+    bool ok[WRB];
+#pragma unroll
+    for (int u = 0; u < WRB; ++u) {
+      int t = t0 + u * WNT + threadIdx.x, r = 0;
+      ok[u] = t < ntiles;
+      if (!ok[u]) t = 0;
+      while (t >= nbk - r) {
+        t -= nbk - r;
+        ++r;
+      }
+      ta[u] = r;
+      tb[u] = r + t;
     }
-    const int tb = ta + rem;
-    double acc[4][4];
+    double acc[WRB][4][4];
 #pragma unroll
-    for (int p = 0; p < 4; ++p)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[p][q] = 0.0;
-#pragma unroll 4
-    for (int c = 0; c < n; ++c) {
-      const double4 ja = *(const double4*)(J + (int64_t)c * ld + 4 * ta);
-      const double4 jb = *(const double4*)(J + (int64_t)c * ld + 4 * tb);
-      const double va[4] = {ja.x, ja.y, ja.z, ja.w}, vb[4] = {jb.x, jb.y, jb.z, jb.w};
+    for (int u = 0; u < WRB; ++u)
 #pragma unroll
       for (int p = 0; p < 4; ++p)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc[p][q] = fma(va[p], vb[q], acc[p][q]);
+        for (int q = 0; q < 4; ++q) acc[u][p][q] = 0.0;
+    for (int base = 0; base < n; base += WCH) {
+      const int cnt = min(WCH, n - base);
+      __syncthreads();
+      for (int it = threadIdx.x; it < cnt * h; it += WNT) {  // (row, hidden unit) items
+        const int c = it / h, j = it - c * h;
+        const double* x = X + (int64_t)(base + c) * xs;
+        double pre = 0.0;
+        for (int k = 0; k < d; ++k) pre = fma(__ldg(x + k), S.w[j * d + k], pre);
+        const double a = tansig(__dadd_rn(pre, S.w[hd + j]));
+        const double da = __dmul_rn(__dsub_rn(1.0, __dmul_rn(a, a)), S.w[hd + h + j]);
+        double* row = Jc + c * rw;
+        for (int k = 0; k < d; ++k) row[j * d + k] = __dmul_rn(da, __ldg(x + k));
+        row[hd + j] = da;
+        row[hd + h + j] = a;
+      }
+      __syncthreads();
+      for (int c = threadIdx.x; c < cnt; c += WNT) {  // residual, wide_sample's order
+        double* row = Jc + c * rw;
+        double out = 0.0;
+        for (int j = 0; j < h; ++j) out = fma(row[hd + h + j], S.w[hd + h + j], out);
+        row[hd + 2 * h] = 1.0;
+        row[P] = __dsub_rn(__dadd_rn(out, S.w[hd + 2 * h]), __ldg(Y + base + c));
+        for (int q = P + 1; q < rw; ++q) row[q] = 0.0;
+      }
+      __syncthreads();
+      for (int c = 0; c < cnt; ++c) {
+        const double* row = Jc + c * rw;
+#pragma unroll
+        for (int u = 0; u < WRB; ++u) {
+          if (!ok[u]) continue;
+          const double2 a01 = *(const double2*)(row + 4 * ta[u]);
+          const double2 a23 = *(const double2*)(row + 4 * ta[u] + 2);
+          const double2 b01 = *(const double2*)(row + 4 * tb[u]);
+          const double2 b23 = *(const double2*)(row + 4 * tb[u] + 2);
+          const double va[4] = {a01.x, a01.y, a23.x, a23.y};
+          const double vb[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+          for (int p = 0; p < 4; ++p)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[u][p][q] = fma(va[p], vb[q], acc[u][p][q]);
+        }
+      }
     }
 #pragma unroll
-    for (int p = 0; p < 4; ++p)
+    for (int u = 0; u < WRB; ++u) {
+      if (!ok[u]) continue;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int a = 4 * ta + p, b = 4 * tb + q;
-        jtj[(int64_t)a * ld + b] = acc[p][q];
-        jtj[(int64_t)b * ld + a] = acc[p][q];
-      }
-  }
-  for (int a = threadIdx.x; a < P; a += WNT) {
-    double s = 0.0;
-    for (int c = 0; c < n; ++c) s = fma(J[(int64_t)c * ld + a], R[c], s);
-    S.jtr[a] = s;
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int a = 4 * ta[u] + p, b = 4 * tb[u] + q;
+          if (a > b || a >= P) continue;
+          if (b < P) {
+            jtj[(int64_t)a * ld + b] = acc[u][p][q];
+            jtj[(int64_t)b * ld + a] = acc[u][p][q];
+          } else if (b == P) {
+            S.jtr[a] = acc[u][p][q];
+          }
+        }
+    }
   }
   __syncthreads();
+}
+
+// Damped system by blocked Cholesky (A = beta J'J + (mu+alpha) I is SPD; the
+// north star's "in-shared-memory Cholesky"): 32-column panels -- the diagonal
+// block factored by one warp in shared memory, the panel below solved one row
+// per thread and kept transposed in shared memory, the trailing lower
+// triangle updated with 4x4 register blocks from the panel (one L2 pass per
+// panel).  Blocked forward / backward substitution.  Returns false when a
+// pivot is not positive (numerically indefinite); the caller then runs the
+// LU of the reference (wide_solve).
+constexpr int WNB = 32;
+
+__device__ bool wide_chol(double* A, const double* jtj, int ld, int P, double alpha, double beta,
+                          double mu, WideSmem& S, double* dyn) {
+  const double damp = __dadd_rn(mu, alpha);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rw = wide_rw(P);
+  double* PT = dyn;               // panel, transposed: PT[t * rw + i]
+  double* D = dyn + WNB * rw;     // diagonal block, 32 x 33
+  for (int a = warp; a < P; a += WWARPS)
+    for (int b = lane; b <= a; b += 32) {
+      const double v = __dmul_rn(beta, jtj[(int64_t)a * ld + b]);
+      A[(int64_t)a * ld + b] = (a == b) ? __dadd_rn(v, damp) : v;
+    }
+  for (int a = threadIdx.x; a < P; a += WNT)
+    S.rhs[a] = -__dadd_rn(__dmul_rn(beta, S.jtr[a]), __dmul_rn(alpha, S.w[a]));
+  __syncthreads();
+  for (int kb = 0; kb < P; kb += WNB) {
+    const int nb = min(WNB, P - kb), r0 = kb + nb, m = P - r0;
+    for (int e = threadIdx.x; e < nb * nb; e += WNT) {
+      const int i = e / nb, j = e - i * nb;
+      D[i * 33 + j] = j <= i ? A[(int64_t)(kb + i) * ld + kb + j] : 0.0;
+    }
+    __syncthreads();
+    if (warp == 0) {  // unblocked right-looking Cholesky of the diagonal block
+      bool bad = false;
+      for (int k = 0; k < nb; ++k) {
+        const double dkk = D[k * 33 + k];
+        if (!(dkk > 0.0)) {
+          bad = true;
+          break;
+        }
+        const double sk = sqrt(dkk);
+        __syncwarp();
+        if (lane == k) D[k * 33 + k] = sk;
+        if (lane > k && lane < nb) D[lane * 33 + k] = D[lane * 33 + k] / sk;
+        __syncwarp();
+        if (lane > k && lane < nb) {
+          const double lk = D[lane * 33 + k];
+          for (int j = k + 1; j <= lane; ++j) D[lane * 33 + j] = fma(-lk, D[j * 33 + k], D[lane * 33 + j]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) S.piv = bad ? 1 : 0;
+    }
+    __syncthreads();
+    if (S.piv) return false;
+    for (int e = threadIdx.x; e < nb * nb; e += WNT) {
+      const int i = e / nb, j = e - i * nb;
+      if (j <= i) A[(int64_t)(kb + i) * ld + kb + j] = D[i * 33 + j];
+    }
+    // panel rows below: x = a * L11^-T, one row per thread
+    for (int i = threadIdx.x; i < m; i += WNT) {
+      const double* ai = A + (int64_t)(r0 + i) * ld + kb;
+      double xv[WNB];
+#pragma unroll
+      for (int j = 0; j < WNB; ++j) xv[j] = j < nb ? ai[j] : 0.0;
+#pragma unroll
+      for (int j = 0; j < WNB; ++j) {
+        if (j < nb) {
+          double sacc = xv[j];
+#pragma unroll
+          for (int t = 0; t < j; ++t) sacc = fma(-xv[t], D[j * 33 + t], sacc);
+          xv[j] = sacc / D[j * 33 + j];
+        }
+      }
+      double* ao = A + (int64_t)(r0 + i) * ld + kb;
+#pragma unroll
+      for (int j = 0; j < WNB; ++j)
+        if (j < nb) {
+          ao[j] = xv[j];
+          PT[j * rw + i] = xv[j];
+        }
+    }
+    __syncthreads();
+    // trailing update of the lower triangle: A22 -= X X'
+    const int mb = (m + 3) >> 2;
+    const int nt = mb * (mb + 1) / 2;
+    for (int t = threadIdx.x; t < nt; t += WNT) {
+      int ti = 0, rem = t;  // lower triangle, row-major: (ti >= tj)
+      while (rem > ti) {
+        rem -= ti + 1;
+        ++ti;
+      }
+      const int tj = rem;
+      double acc[4][4];
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = 0.0;
+      for (int k = 0; k < nb; ++k) {
+        const double* pk = PT + k * rw;
+        double va[4], vb[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          va[p] = 4 * ti + p < m ? pk[4 * ti + p] : 0.0;
+          vb[p] = 4 * tj + p < m ? pk[4 * tj + p] : 0.0;
+        }
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[p][q] = fma(va[p], vb[q], acc[p][q]);
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = 4 * ti + p, j = 4 * tj + q;
+          if (i < m && j <= i) {
+            double* a = A + (int64_t)(r0 + i) * ld + r0 + j;
+            *a = *a - acc[p][q];
+          }
+        }
+    }
+    __syncthreads();
+  }
+  auto load_diag = [&](int kb, int nb) {  // factored diagonal block -> D (shared)
+    for (int e = threadIdx.x; e < nb * nb; e += WNT) {
+      const int i = e / nb, j = e - i * nb;
+      D[i * 33 + j] = j <= i ? A[(int64_t)(kb + i) * ld + kb + j] : 0.0;
+    }
+  };
+  // forward: L y = b
+  for (int kb = 0; kb < P; kb += WNB) {
+    const int nb = min(WNB, P - kb), r0 = kb + nb;
+    load_diag(kb, nb);
+    __syncthreads();
+    if (warp == 0) {
+      double b = lane < nb ? S.rhs[kb + lane] : 0.0;
+      for (int k = 0; k < nb; ++k) {
+        double yk = lane == k ? b / D[k * 33 + k] : 0.0;
+        yk = __shfl_sync(0xffffffffu, yk, k);
+        if (lane == k) b = yk;
+        if (lane > k && lane < nb) b = fma(-D[lane * 33 + k], yk, b);
+      }
+      if (lane < nb) S.rhs[kb + lane] = b;
+    }
+    __syncthreads();
+    for (int i = r0 + threadIdx.x; i < P; i += WNT) {
+      const double* li = A + (int64_t)i * ld + kb;
+      double sacc = S.rhs[i];
+      for (int t = 0; t < nb; ++t) sacc = fma(-li[t], S.rhs[kb + t], sacc);
+      S.rhs[i] = sacc;
+    }
+    __syncthreads();
+  }
+  // backward: L' x = y
+  const int nblk = (P + WNB - 1) / WNB;
+  for (int bi = nblk - 1; bi >= 0; --bi) {
+    const int kb = bi * WNB, nb = min(WNB, P - kb), r0 = kb + nb;
+    {  // y_block -= L(r0:, block)' x(r0:): column c = lane, rows split over warps
+      double part = 0.0;
+      if (lane < nb)
+        for (int i = r0 + warp; i < P; i += WWARPS) part = fma(A[(int64_t)i * ld + kb + lane], S.delta[i], part);
+      S.v[warp * 32 + lane] = part;
+    }
+    load_diag(kb, nb);
+    __syncthreads();
+    if (warp == 0) {
+      double b = 0.0;
+      if (lane < nb) {
+        b = S.rhs[kb + lane];
+        double tot = 0.0;
+        for (int w = 0; w < WWARPS; ++w) tot += S.v[w * 32 + lane];
+        b -= tot;
+      }
+      for (int k = nb - 1; k >= 0; --k) {
+        double xk = lane == k ? b / D[k * 33 + k] : 0.0;
+        xk = __shfl_sync(0xffffffffu, xk, k);
+        if (lane == k) b = xk;
+        if (lane < k) b = fma(-D[k * 33 + lane], xk, b);
+      }
+      if (lane < nb) S.delta[kb + lane] = b;
+    }
+    __syncthreads();
+  }
+  return true;
 }
 
 // LU with partial pivoting on A = beta J'J + (mu+alpha) I; false on a zero pivot
@@ -380,6 +621,7 @@ __global__ void __launch_bounds__(WNT) lm_wide_kernel(WideLaunch L) {
   const int task = blockIdx.x;
   if (task >= L.n_tasks) return;
   __shared__ WideSmem S;
+  extern __shared__ __align__(16) double wdyn[];  // [J r] chunk / Cholesky panel + block
   const bbml_lm_task tk = L.tasks[task];
   const int orig = L.orig_index[task];
   const int n = tk.n, d = tk.d, h = tk.h;
@@ -390,8 +632,6 @@ __global__ void __launch_bounds__(WNT) lm_wide_kernel(WideLaunch L) {
   double* slab = L.scratch + (int64_t)blockIdx.x * L.slab_doubles;
   double* jtj = slab;
   double* A = jtj + (int64_t)ld * ld;
-  double* R = A + (int64_t)ld * ld;
-  double* J = R + ((n + 3) & ~3);
 
   if (threadIdx.x == 0) {
     Pcg64 rng;
@@ -417,7 +657,7 @@ __global__ void __launch_bounds__(WNT) lm_wide_kernel(WideLaunch L) {
   for (int ep = 0; ep < tk.max_epochs; ++ep) {
     if (!have_stats) {
       WP_T(t0);
-      wide_stats(J, R, jtj, ld, X, Y, n, d, h, P, xs, S);
+      wide_stats_chunked(jtj, ld, X, Y, n, d, h, P, xs, S, wdyn);
       WP_ADD(0, t0);
     }
     const double f0 = __dadd_rn(__dmul_rn(beta, e_d), __dmul_rn(alpha, e_w));
@@ -426,7 +666,8 @@ __global__ void __launch_bounds__(WNT) lm_wide_kernel(WideLaunch L) {
     while (true) {
       ++trials;
       WP_T(t2);
-      const bool solved = wide_solve(A, jtj, ld, P, alpha, beta, mu, S);
+      bool solved = wide_chol(A, jtj, ld, P, alpha, beta, mu, S, wdyn);
+      if (!solved) solved = wide_solve(A, jtj, ld, P, alpha, beta, mu, S);  // indefinite: LU
       WP_ADD(2, t2);
       if (!solved) {
         code = BBML_MODEL_SINGULAR;
@@ -460,7 +701,7 @@ __global__ void __launch_bounds__(WNT) lm_wide_kernel(WideLaunch L) {
     int pinned = 0;
     if (est) {
       WP_T(t0);
-      wide_stats(J, R, jtj, ld, X, Y, n, d, h, P, xs, S);
+      wide_stats_chunked(jtj, ld, X, Y, n, d, h, P, xs, S, wdyn);
       WP_ADD(0, t0);
       have_stats = true;
       WP_T(t1);
@@ -540,7 +781,10 @@ bbml_status lm_wide_launch(const bbml_lm_task* d_tasks, const int32_t* d_orig,
     nmax = std::max(nmax, h_tasks[i].n);
   }
   const int ld = (pmax + 3) & ~3;
-  const int64_t slab = 2 * (int64_t)ld * ld + ((nmax + 3) & ~3) + (int64_t)nmax * ld;
+  const int64_t slab = 2 * (int64_t)ld * ld;  // J'J + factorisation workspace
+  const int rw = (pmax + 1 + 3) & ~3;
+  const size_t dyn = (size_t)(WNB * rw + 32 * 33) * sizeof(double);
+  (void)nmax;
   if (alloc_only) return scratch.alloc(slabs, slab * n_tasks);
   double* d_scratch = *slabs;
   WideLaunch L{};
@@ -556,7 +800,11 @@ bbml_status lm_wide_launch(const bbml_lm_task* d_tasks, const int32_t* d_orig,
   L.scratch = d_scratch;
   L.slab_doubles = slab;
   L.ld = ld;
-  lm_wide_kernel<<<n_tasks, WNT, 0, s>>>(L);
+  static_assert(WCH == WNB, "chunk rows and panel width share the dynamic buffer");
+  cudaError_t ea = cudaFuncSetAttribute(lm_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)dyn);
+  if (ea != cudaSuccess) return cuda_status(ea, "lm_wide smem");
+  lm_wide_kernel<<<n_tasks, WNT, dyn, s>>>(L);
   cudaError_t e = cudaGetLastError();
 #ifdef BBML_LM_PROF
   {
