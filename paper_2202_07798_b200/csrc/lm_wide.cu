@@ -519,72 +519,120 @@ __device__ bool wide_solve(double* A, const double* jtj, int ld, int P, double a
 }
 
 // gamma = sum beta*l/(beta*l+alpha) over the eigenvalues of J'J (clipped at 0)
-__device__ double wide_gamma(double* A, const double* jtj, int ld, int P, double alpha, double beta,
-                             WideSmem& S) {
+// Householder tridiagonalisation (dsytrd, lower) of the symmetric J'J, one
+// pass over the trailing lower triangle per step: the rank-2 update of step
+// k-1 (A -= v w' + w v') is applied in the same sweep that forms p = A v of
+// step k (row dot products by warp reductions, the transposed half by
+// per-lane column partials reduced across warps), so each element is read
+// and written once per step instead of read twice and written once, and only
+// the lower triangle is touched.  Leaves diag / off-diag in S.dd / S.ee.
+constexpr int WCOLS = WPMAX / 32;  // column partials per lane
+
+__device__ void wide_tridiag(double* A, const double* jtj, int ld, int P, WideSmem& S, double* dyn) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* vp = S.v;    // pending reflector (step k-1)
+  double* wp = S.pv;   // pending rank-2 partner
+  double* vn = S.e2;   // reflector of step k (e2 is free until the Sturm stage)
+  double* rowp = S.wt; // row dot products (wt is free during the evidence update)
+  double* colp = dyn;  // WWARPS x P column partials
   for (int a = warp; a < P; a += WWARPS)
-    for (int b = lane; b < P; b += 32) A[(int64_t)a * ld + b] = jtj[(int64_t)a * ld + b];
+    for (int b = lane; b <= a; b += 32) A[(int64_t)a * ld + b] = jtj[(int64_t)a * ld + b];
+  bool pend = false;
   __syncthreads();
   for (int k = 0; k + 2 < P; ++k) {
+    // column k (rows >= k) brought up to date with the pending update
     double part = 0.0;
-    for (int i = k + 1 + threadIdx.x; i < P; i += WNT) {
-      const double xi = A[(int64_t)i * ld + k];
-      part = fma(xi, xi, part);
+    for (int i = k + threadIdx.x; i < P; i += WNT) {
+      double* a = A + (int64_t)i * ld + k;
+      double x = *a;
+      if (pend) {
+        x -= fma(vp[i], wp[k], wp[i] * vp[k]);
+        *a = x;
+      }
+      if (i > k) part = fma(x, x, part);
     }
     const double sig = bsum(part, S);
     const double x0 = A[(int64_t)(k + 1) * ld + k];
-    const double tail = sig - x0 * x0;
-    if (!(tail > 0.0)) {
-      if (threadIdx.x == 0) S.ee[k] = x0;
-      __syncthreads();
-      continue;
-    }
+    const double akk = A[(int64_t)k * ld + k];
+    const bool refl = sig - x0 * x0 > 0.0;
     const double al = x0 > 0.0 ? -sqrt(sig) : sqrt(sig);
-    const double bh = 1.0 / (sig - al * x0);
+    const double bh = refl ? 1.0 / (sig - al * x0) : 0.0;
     for (int i = k + 1 + threadIdx.x; i < P; i += WNT)
-      S.v[i] = A[(int64_t)i * ld + k] - (i == k + 1 ? al : 0.0);
+      vn[i] = refl ? A[(int64_t)i * ld + k] - (i == k + 1 ? al : 0.0) : 0.0;
+    if (threadIdx.x == 0) {
+      S.dd[k] = akk;
+      S.ee[k] = refl ? al : x0;
+    }
     __syncthreads();
-    for (int i = k + 1 + warp; i < P; i += WWARPS) {  // p = bh * A v (warp per row)
-      const double* __restrict__ ai = A + (int64_t)i * ld;
-      double p = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-      int j = k + 1 + lane;
-      for (; j + 96 < P; j += 128) {
-        p = fma(ai[j], S.v[j], p);
-        p1 = fma(ai[j + 32], S.v[j + 32], p1);
-        p2 = fma(ai[j + 64], S.v[j + 64], p2);
-        p3 = fma(ai[j + 96], S.v[j + 96], p3);
-      }
-      for (; j < P; j += 32) p = fma(ai[j], S.v[j], p);
-      p = (p + p1) + (p2 + p3);
+    // fused sweep over the trailing lower triangle (rows/cols > k)
+    double cacc[WCOLS];
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-      if (lane == 0) S.pv[i] = p * bh;
+    for (int t = 0; t < WCOLS; ++t) cacc[t] = 0.0;
+    for (int i = k + 1 + warp; i < P; i += WWARPS) {
+      double* ai = A + (int64_t)i * ld;
+      const double vpi = pend ? vp[i] : 0.0, wpi = pend ? wp[i] : 0.0, vni = vn[i];
+      double racc = 0.0;
+#pragma unroll
+      for (int t = 0; t < WCOLS; ++t) {
+        const int j = k + 1 + lane + 32 * t;
+        if (j <= i) {
+          double a = ai[j];
+          if (pend) {
+            a -= fma(vpi, wp[j], wpi * vp[j]);
+            ai[j] = a;
+          }
+          racc = fma(a, vn[j], racc);
+          if (j < i) cacc[t] = fma(a, vni, cacc[t]);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, o);
+      if (lane == 0) rowp[i] = racc;
+    }
+#pragma unroll
+    for (int t = 0; t < WCOLS; ++t) {
+      const int j = k + 1 + lane + 32 * t;
+      if (j < P) colp[warp * P + j] = cacc[t];
     }
     __syncthreads();
     double kp = 0.0;
-    for (int i = k + 1 + threadIdx.x; i < P; i += WNT) kp = fma(S.v[i], S.pv[i], kp);
-    const double K = 0.5 * bh * bsum(kp, S);
-    for (int i = k + 1 + threadIdx.x; i < P; i += WNT) S.pv[i] = S.pv[i] - K * S.v[i];
-    __syncthreads();
-    for (int i = k + 1 + warp; i < P; i += WWARPS) {  // A -= v w' + w v'
-      double* __restrict__ ai = A + (int64_t)i * ld;
-      const double vi = S.v[i], wi = S.pv[i];
-      int j = k + 1 + lane;
-      for (; j + 96 < P; j += 128) {
-        const double a0 = ai[j], a1 = ai[j + 32], a2 = ai[j + 64], a3 = ai[j + 96];
-        ai[j] = a0 - fma(vi, S.pv[j], wi * S.v[j]);
-        ai[j + 32] = a1 - fma(vi, S.pv[j + 32], wi * S.v[j + 32]);
-        ai[j + 64] = a2 - fma(vi, S.pv[j + 64], wi * S.v[j + 64]);
-        ai[j + 96] = a3 - fma(vi, S.pv[j + 96], wi * S.v[j + 96]);
-      }
-      for (; j < P; j += 32) ai[j] -= fma(vi, S.pv[j], wi * S.v[j]);
+    for (int i = k + 1 + threadIdx.x; i < P; i += WNT) {
+      double pi = rowp[i];
+#pragma unroll
+      for (int w = 0; w < WWARPS; ++w) pi += colp[w * P + i];
+      pi *= bh;
+      rowp[i] = pi;
+      kp = fma(vn[i], pi, kp);
     }
-    if (threadIdx.x == 0) S.ee[k] = al;
+    const double K = 0.5 * bh * bsum(kp, S);
+    for (int i = k + 1 + threadIdx.x; i < P; i += WNT) {
+      wp[i] = rowp[i] - K * vn[i];
+      vp[i] = vn[i];
+    }
+    if (threadIdx.x == 0) {  // entries <= k of the new pending vectors are unused
+      vp[k] = 0.0;
+      wp[k] = 0.0;
+    }
+    pend = refl;
     __syncthreads();
   }
-  for (int i = threadIdx.x; i < P; i += WNT) S.dd[i] = A[(int64_t)i * ld + i];
-  if (threadIdx.x == 0 && P >= 2) S.ee[P - 2] = A[(int64_t)(P - 1) * ld + (P - 2)];
+  // last 2x2 block
+  if (threadIdx.x < 3) {
+    const int i = P - 2 + (threadIdx.x > 0), j = P - 2 + (threadIdx.x > 1);
+    double* a = A + (int64_t)(threadIdx.x == 1 ? P - 1 : i) * ld + (threadIdx.x == 1 ? P - 2 : j);
+    const int ii = threadIdx.x == 1 ? P - 1 : i, jj = threadIdx.x == 1 ? P - 2 : j;
+    double x = *a;
+    if (pend) x -= fma(vp[ii], wp[jj], wp[ii] * vp[jj]);
+    if (threadIdx.x == 0) S.dd[P - 2] = x;
+    else if (threadIdx.x == 1) S.ee[P - 2] = x;
+    else S.dd[P - 1] = x;
+  }
   __syncthreads();
+}
+
+__device__ double wide_gamma(double* A, const double* jtj, int ld, int P, double alpha, double beta,
+                             WideSmem& S, double* dyn) {
+  wide_tridiag(A, jtj, ld, P, S, dyn);
   WP_T(tb);
   double glo = 1e308, ghi = -1e308;
   for (int i = threadIdx.x; i < P; i += WNT) {
@@ -705,7 +753,7 @@ __global__ void __launch_bounds__(WNT) lm_wide_kernel(WideLaunch L) {
       WP_ADD(0, t0);
       have_stats = true;
       WP_T(t1);
-      gamma = wide_gamma(A, jtj, ld, P, alpha, beta, S);
+      gamma = wide_gamma(A, jtj, ld, P, alpha, beta, S, wdyn);
       WP_ADD(1, t1);
       double na, nb;
       if (e_w > 0.0) {
