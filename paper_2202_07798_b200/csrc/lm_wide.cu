@@ -571,12 +571,17 @@ __device__ void wide_tridiag(double* A, const double* jtj, int ld, int P, WideSm
     for (int i = k + 1 + warp; i < P; i += WWARPS) {
       double* ai = A + (int64_t)i * ld;
       const double vpi = pend ? vp[i] : 0.0, wpi = pend ? wp[i] : 0.0, vni = vn[i];
-      double racc = 0.0;
+      double racc = 0.0, av[WCOLS];
+#pragma unroll
+      for (int t = 0; t < WCOLS; ++t) {  // all loads of the row segment in flight first
+        const int j = k + 1 + lane + 32 * t;
+        av[t] = j <= i ? ai[j] : 0.0;
+      }
 #pragma unroll
       for (int t = 0; t < WCOLS; ++t) {
         const int j = k + 1 + lane + 32 * t;
         if (j <= i) {
-          double a = ai[j];
+          double a = av[t];
           if (pend) {
             a -= fma(vpi, wp[j], wpi * vp[j]);
             ai[j] = a;
