@@ -121,50 +121,61 @@ __device__ double wide_energy(const double* wv, const double* X, const double* Y
   return bsum(acc, S);
 }
 
-// J'J and J'r without a Jacobian slab: rows of [J | r] are generated 32 at a
-// time into shared memory (one (row, hidden unit) item per thread, then the
-// residual per row in the reference's summation order) and every thread
-// accumulates 4x4 register blocks of the upper triangle of [J r]'[J r] over
-// all rows (sample order: the same order and rounding as the per-entry sum).
-// Three register blocks per thread per pass; passes regenerate the chunk.
+// [J r] rows are generated 32 at a time into shared memory (no Jacobian in
+// HBM): one (row, hidden unit) item per thread, then the residual per row in
+// the reference's summation order.
 constexpr int WCH = 32;  // staged rows per chunk
-constexpr int WRB = 3;   // 4x4 blocks per thread per pass
 
-__device__ __forceinline__ int wide_rw(int P) { return (P + 1 + 3) & ~3; }
+// staged row width: P J columns + r, padded to 8-column tiles and to 8 (mod
+// 16) doubles so that the DMMA fragment loads (4 rows x 8 columns per warp)
+// take the minimum two shared-memory wavefronts
+__device__ __host__ __forceinline__ int wide_rw(int P) {
+  const int w = (P + 1 + 7) & ~7;
+  return (w & 15) ? w : w + 8;
+}
 
-__device__ void wide_stats_chunked(double* jtj, int ld, const double* X, const double* Y, int n, int d,
-                                   int h, int P, int xs, WideSmem& S, double* Jc) {
-  const int rw = wide_rw(P);  // row width: P J columns, r, zero pad
-  const int nbk = rw / 4;
-  const int ntiles = nbk * (nbk + 1) / 2;
+// J'J and J'r on the FP64 tensor cores (BASELINE cfg 5): the same staged
+// [J r] chunks, the upper triangle of [J r]'[J r] in 8x8 tiles, one
+// mma.sync.m8n8k4.f64 per tile and 4 staged rows (A fragment = tile row block,
+// B fragment = tile column block of the same 4 rows).  Each warp owns a run
+// of up to WCAP consecutive tiles of the row-major upper-triangle list (so
+// the A fragment is reused along the run); accumulators stay in registers
+// across all chunks.
+constexpr int WCAP = 36;
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ void wide_stats_dmma(double* jtj, int ld, const double* X, const double* Y, int n, int d,
+                                int h, int P, int xs, WideSmem& S, double* Jc) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rw = wide_rw(P);
+  const int nt = (P + 1 + 7) / 8;
+  const int npair = nt * (nt + 1) / 2;
   const int hd = h * d;
-  const int per_pass = WNT * WRB;
-  for (int t0 = 0; t0 < ntiles; t0 += per_pass) {
-    int ta[WRB], tb[WRB];
-    bool ok[WRB];
-#pragma unroll
-    for (int u = 0; u < WRB; ++u) {
-      int t = t0 + u * WNT + threadIdx.x, r = 0;
-      ok[u] = t < ntiles;
-      if (!ok[u]) t = 0;
-      while (t >= nbk - r) {
-        t -= nbk - r;
-        ++r;
+  for (int p0 = 0; p0 < npair; p0 += WWARPS * WCAP) {
+    const int first = p0 + warp * WCAP;
+    const int cnt = max(0, min(WCAP, npair - first));
+    int ta0 = 0, tb0 = 0;
+    {
+      int t = cnt > 0 ? first : 0;
+      while (t >= nt - ta0) {
+        t -= nt - ta0;
+        ++ta0;
       }
-      ta[u] = r;
-      tb[u] = r + t;
+      tb0 = ta0 + t;
     }
-    double acc[WRB][4][4];
+    double acc[WCAP][2];
 #pragma unroll
-    for (int u = 0; u < WRB; ++u)
-#pragma unroll
-      for (int p = 0; p < 4; ++p)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[u][p][q] = 0.0;
+    for (int q = 0; q < WCAP; ++q) acc[q][0] = acc[q][1] = 0.0;
     for (int base = 0; base < n; base += WCH) {
-      const int cnt = min(WCH, n - base);
+      const int rows = min(WCH, n - base);
+      const int rows4 = (rows + 3) & ~3;
       __syncthreads();
-      for (int it = threadIdx.x; it < cnt * h; it += WNT) {  // (row, hidden unit) items
+      for (int it = threadIdx.x; it < rows * h; it += WNT) {  // (row, hidden unit) items
         const int c = it / h, j = it - c * h;
         const double* x = X + (int64_t)(base + c) * xs;
         double pre = 0.0;
@@ -176,8 +187,9 @@ __device__ void wide_stats_chunked(double* jtj, int ld, const double* X, const d
         row[hd + j] = da;
         row[hd + h + j] = a;
       }
+      for (int e = rows * rw + threadIdx.x; e < rows4 * rw; e += WNT) Jc[e] = 0.0;  // pad rows
       __syncthreads();
-      for (int c = threadIdx.x; c < cnt; c += WNT) {  // residual, wide_sample's order
+      for (int c = threadIdx.x; c < rows; c += WNT) {  // residual, wide_sample's order
         double* row = Jc + c * rw;
         double out = 0.0;
         for (int j = 0; j < h; ++j) out = fma(row[hd + h + j], S.w[hd + h + j], out);
@@ -186,40 +198,47 @@ __device__ void wide_stats_chunked(double* jtj, int ld, const double* X, const d
         for (int q = P + 1; q < rw; ++q) row[q] = 0.0;
       }
       __syncthreads();
-      for (int c = 0; c < cnt; ++c) {
-        const double* row = Jc + c * rw;
+      if (cnt > 0) {
+        for (int ks = 0; ks < rows4; ks += 4) {
+          const double* fr = Jc + (ks + (lane & 3)) * rw + (lane >> 2);
+          int ta = ta0, tb = tb0;
+          double fa = fr[8 * ta];
 #pragma unroll
-        for (int u = 0; u < WRB; ++u) {
-          if (!ok[u]) continue;
-          const double2 a01 = *(const double2*)(row + 4 * ta[u]);
-          const double2 a23 = *(const double2*)(row + 4 * ta[u] + 2);
-          const double2 b01 = *(const double2*)(row + 4 * tb[u]);
-          const double2 b23 = *(const double2*)(row + 4 * tb[u] + 2);
-          const double va[4] = {a01.x, a01.y, a23.x, a23.y};
-          const double vb[4] = {b01.x, b01.y, b23.x, b23.y};
-#pragma unroll
-          for (int p = 0; p < 4; ++p)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[u][p][q] = fma(va[p], vb[q], acc[u][p][q]);
+          for (int q = 0; q < WCAP; ++q) {
+            if (q < cnt) {
+              dmma884(acc[q], fa, fr[8 * tb]);
+              if (++tb == nt) {
+                ++ta;
+                tb = ta;
+                if (ta < nt) fa = fr[8 * ta];
+              }
+            }
+          }
         }
       }
     }
+    int ta = ta0, tb = tb0;
 #pragma unroll
-    for (int u = 0; u < WRB; ++u) {
-      if (!ok[u]) continue;
+    for (int q = 0; q < WCAP; ++q) {
+      if (q < cnt) {
+        const int a = 8 * ta + (lane >> 2);
 #pragma unroll
-      for (int p = 0; p < 4; ++p)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int a = 4 * ta[u] + p, b = 4 * tb[u] + q;
-          if (a > b || a >= P) continue;
-          if (b < P) {
-            jtj[(int64_t)a * ld + b] = acc[u][p][q];
-            jtj[(int64_t)b * ld + a] = acc[u][p][q];
-          } else if (b == P) {
-            S.jtr[a] = acc[u][p][q];
+        for (int i = 0; i < 2; ++i) {
+          const int b = 8 * tb + 2 * (lane & 3) + i;
+          if (a <= b && a < P) {
+            if (b < P) {
+              jtj[(int64_t)a * ld + b] = acc[q][i];
+              jtj[(int64_t)b * ld + a] = acc[q][i];
+            } else if (b == P) {
+              S.jtr[a] = acc[q][i];
+            }
           }
         }
+        if (++tb == nt) {
+          ++ta;
+          tb = ta;
+        }
+      }
     }
   }
   __syncthreads();
@@ -710,7 +729,7 @@ __global__ void __launch_bounds__(WNT) lm_wide_kernel(WideLaunch L) {
   for (int ep = 0; ep < tk.max_epochs; ++ep) {
     if (!have_stats) {
       WP_T(t0);
-      wide_stats_chunked(jtj, ld, X, Y, n, d, h, P, xs, S, wdyn);
+      wide_stats_dmma(jtj, ld, X, Y, n, d, h, P, xs, S, wdyn);
       WP_ADD(0, t0);
     }
     const double f0 = __dadd_rn(__dmul_rn(beta, e_d), __dmul_rn(alpha, e_w));
@@ -754,7 +773,7 @@ __global__ void __launch_bounds__(WNT) lm_wide_kernel(WideLaunch L) {
     int pinned = 0;
     if (est) {
       WP_T(t0);
-      wide_stats_chunked(jtj, ld, X, Y, n, d, h, P, xs, S, wdyn);
+      wide_stats_dmma(jtj, ld, X, Y, n, d, h, P, xs, S, wdyn);
       WP_ADD(0, t0);
       have_stats = true;
       WP_T(t1);
@@ -835,7 +854,7 @@ bbml_status lm_wide_launch(const bbml_lm_task* d_tasks, const int32_t* d_orig,
   }
   const int ld = (pmax + 3) & ~3;
   const int64_t slab = 2 * (int64_t)ld * ld;  // J'J + factorisation workspace
-  const int rw = (pmax + 1 + 3) & ~3;
+  const int rw = wide_rw(pmax);
   const size_t dyn = (size_t)(WNB * rw + 32 * 33) * sizeof(double);
   (void)nmax;
   if (alloc_only) return scratch.alloc(slabs, slab * n_tasks);
