@@ -254,7 +254,10 @@ __device__ void perm_producer_warp(const PnnLaunch& L, int groups, int pw, int n
       progress = true;
     }
     if (!alive) break;
-    if (!progress) __nanosleep(100);
+    // waiting for a consumer (it needs ~1 ms per epoch of a long series):
+    // poll rarely so the idle producer does not take issue slots from the
+    // consumer warp on the same SM sub-partition
+    if (!progress) __nanosleep(2000);
   }
 }
 
