@@ -1178,9 +1178,10 @@ __global__ void __launch_bounds__(128) lm_warp_kernel(LmLaunch L) {
       LM_PROF_ADD(0, t0);
       have_stats = true;
       LM_PROF_T(t1);
-      // P <= 8: cyclic Jacobi (measured: tridiagonal + bisection is not
-      // faster at this size and shifts early-stop epochs)
+      // P <= 5: cyclic Jacobi (converges in a few sweeps at this size);
+      // P >= 6: Householder + bisection
       if constexpr (WarpLm<PM>::kWide) gamma = w_gamma_tri<PM>(S, P, alpha, beta, lane);
+      else if (P >= 6) gamma = w_gamma_tri<PM>(S, P, alpha, beta, lane);
       else gamma = w_gamma<PM>(S, P, alpha, beta, lane);
       LM_PROF_ADD(1, t1);
       double na, nb;
