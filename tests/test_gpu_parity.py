@@ -300,3 +300,34 @@ def test_learning_curves_batched_match_oracle(tmp_path):
     man = json.loads((tmp_path / "sweep_manifest.json").read_text())
     assert man["curves"] == 6 and man["fractions"] == sorted(fr)
     assert len(list(tmp_path.glob("curve_*.csv"))) == 6
+
+
+def test_br_wide_accuracy_parity_hidden64():
+    """BASELINE cfg 5 (hidden 64, P = 257) on the device's wide path: accuracy
+    parity with the oracle within the north-star +-0.5 pp over ten app20
+    series (HighLow split, 100 training rows, 60 LM epochs), plus per-series
+    agreement of the test MSE within 0.05 (the trajectories are near-chaotic,
+    SURVEY §8c)."""
+    from paper_2202_07798_b200 import synth
+    from paper_2202_07798_b200.experiment import ExperimentConfig, train_many
+    from paper_2202_07798_b200.traces import BbSeries, SplitMode
+
+    raw = synth.app20()[:10]
+    series = [BbSeries(k, X, y) for k, X, y in raw]
+    cfg = ExperimentConfig(split_mode=SplitMode.HIGH_LOW, seed=0, br_hidden=64, br_max_epochs=60,
+                           models=("brbpnn",))
+    res = train_many([(s, "brbpnn") for s in series], cfg).results
+    dev, ora = [], []
+    for (k, X, y), r in zip(raw, res):
+        o = O.train_one(k, X, y, "brbpnn", mode="high-low", base_seed=0, br_hidden=64,
+                        br_max_epochs=60)
+        assert (r.error is None) == (o.error is None), (k, r.error, o.error)
+        if r.error is None:
+            dev.append(r.mse)
+            ora.append(o.mse)
+            assert abs(r.mse - o.mse) <= 0.05, (k, r.mse, o.mse)
+    assert len(dev) >= 8
+    acc_dev = 100 * (1 - float(np.mean(dev)))
+    acc_ora = 100 * (1 - float(np.mean(ora)))
+    print("hidden-64 accuracy device %.3f oracle %.3f" % (acc_dev, acc_ora))
+    assert abs(acc_dev - acc_ora) <= 0.5
