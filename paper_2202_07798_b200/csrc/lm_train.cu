@@ -532,21 +532,25 @@ __device__ double w_energy(const WarpLm<PM>& S, const double* wv, const double* 
   if constexpr (D > 0) {
     H1<D> m;
     m.load(wv);
-    // 4 samples per lane per iteration: independent exp/div chains (ILP);
-    // the accumulation order stays the sample order of the lane
-    constexpr int U4 = 4;
+    // 8 samples per lane per iteration, all loads issued first (L2 latency)
+    // then independent exp/div chains (ILP); the accumulation order stays the
+    // sample order of the lane
+    constexpr int U8 = 8;
     int i = lane;
-    for (; i + 32 * (U4 - 1) < n; i += 32 * U4) {
-      double r[U4];
+    for (; i + 32 * (U8 - 1) < n; i += 32 * U8) {
+      double xv[U8][D], yv[U8], r[U8];
 #pragma unroll
-      for (int u = 0; u < U4; ++u) {
-        double x[D];
-        load_x<D>(x, X, i + 32 * u, xs);
-        double a;
-        r[u] = __dsub_rn(m.out(x, a), __ldg(Y + i + 32 * u));
+      for (int u = 0; u < U8; ++u) {
+        load_x<D>(xv[u], X, i + 32 * u, xs);
+        yv[u] = __ldg(Y + i + 32 * u);
       }
 #pragma unroll
-      for (int u = 0; u < U4; ++u) acc = fma(r[u], r[u], acc);
+      for (int u = 0; u < U8; ++u) {
+        double a;
+        r[u] = __dsub_rn(m.out(xv[u], a), yv[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U8; ++u) acc = fma(r[u], r[u], acc);
     }
     for (; i < n; i += 32) {
       double x[D];
@@ -666,11 +670,12 @@ __device__ void w_stats(WarpLm<PM>& S, const double* X, const double* Y, int n, 
     double acc[NA];
 #pragma unroll
     for (int e = 0; e < NA; ++e) acc[e] = 0.0;
-    for (int i = lane; i < n; i += 32) {
-      double x[D];
-      load_x<D>(x, X, i, xs);
+    // per sample: residual, Jacobian row, rank-1 update of [J'J | J'r] in the
+    // lane's sample order; samples in blocks of 4 with every load of the block
+    // issued first (L2 latency) and the four exp/div chains independent
+    auto sample = [&](const double (&x)[D], double yv) {
       double a;
-      const double r = __dsub_rn(m.out(x, a), __ldg(Y + i));
+      const double r = __dsub_rn(m.out(x, a), yv);
       const double g = __dmul_rn(__dsub_rn(1.0, __dmul_rn(a, a)), m.w2);
       double jr[PP];
 #pragma unroll
@@ -685,6 +690,23 @@ __device__ void w_stats(WarpLm<PM>& S, const double* X, const double* Y, int n, 
         for (int q = p; q < PP; ++q, ++e) acc[e] = fma(jr[p], jr[q], acc[e]);
 #pragma unroll
       for (int p = 0; p < PP; ++p, ++e) acc[e] = fma(jr[p], r, acc[e]);
+    };
+    constexpr int UB = 4;
+    int i = lane;
+    for (; i + 32 * (UB - 1) < n; i += 32 * UB) {
+      double xv[UB][D], yv[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        load_x<D>(xv[u], X, i + 32 * u, xs);
+        yv[u] = __ldg(Y + i + 32 * u);
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u) sample(xv[u], yv[u]);
+    }
+    for (; i < n; i += 32) {
+      double x[D];
+      load_x<D>(x, X, i, xs);
+      sample(x, __ldg(Y + i));
     }
     int e = 0;
 #pragma unroll
