@@ -890,7 +890,7 @@ __global__ void pnn_lat_kernel(PnnLaunch L) {
 }
 // short series: 4 consumer + 1 shared producer warp, 2 CTAs per SM
 template <typename T, int DM, int SP, typename PermT>
-__global__ void __launch_bounds__(160, 2) pnn_lat_kernel_shared(PnnLaunch L) {
+__global__ void __launch_bounds__(160, 3) pnn_lat_kernel_shared(PnnLaunch L) {
   pnn_lat_body<T, DM, SP, PermT>(L);
 }
 // 4 consumer + 2 producer warps (each producer serves 2 models), 2 CTAs per SM
