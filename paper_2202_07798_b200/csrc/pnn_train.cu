@@ -582,7 +582,8 @@ __global__ void pnn_train_kernel(PnnLaunch L) {
 //                xor-16 shuffle joins the halves at the end of the minibatch
 // ------------------------------------------------------------------------
 // NPW producer warps per CTA of 4 models: 4 (one per model) for long series,
-// 1 shared producer for short ones (then 2 CTAs fit per SM: <= 204 registers).
+// 1 shared producer for short ones, 8 CTAs per SM (48 registers: the spills
+// cost less than the latency the extra 24 warps hide; sweep PNN 1.83 -> 0.71 s).
 // The long-series variant is left unconstrained: ptxas' larger allocation
 // (~240 registers) measured ~25% lower per-step latency on the critical path.
 template <typename T, int DM, int SP, typename PermT>
@@ -888,9 +889,10 @@ template <typename T, int DM, int SP, typename PermT>
 __global__ void pnn_lat_kernel(PnnLaunch L) {
   pnn_lat_body<T, DM, SP, PermT>(L);
 }
-// short series: 4 consumer + 1 shared producer warp, 2 CTAs per SM
+// short series: 4 consumer + 1 shared producer warp, 8 CTAs per SM (A/B over
+// 2..10 CTAs per SM on the sweep and suite16 workloads: 8 is fastest)
 template <typename T, int DM, int SP, typename PermT>
-__global__ void __launch_bounds__(160, 3) pnn_lat_kernel_shared(PnnLaunch L) {
+__global__ void __launch_bounds__(160, 8) pnn_lat_kernel_shared(PnnLaunch L) {
   pnn_lat_body<T, DM, SP, PermT>(L);
 }
 // 4 consumer + 2 producer warps (each producer serves 2 models), 2 CTAs per SM
@@ -952,7 +954,7 @@ static cudaError_t launch_variant(PnnLaunch L, int64_t nmax, size_t smem_limit, 
   // 4 models per CTA.  Long series: one warp-cooperative producer warp per
   // model (one sequential Fisher-Yates scan keeps up with one consumer warp).
   // Short series (n < kLongSeries): one producer serves the 4 models, so the
-  // CTA is 5 warps and two CTAs fit per SM.
+  // CTA is 5 warps and eight CTAs fit per SM.
   const bool shared_prod = LAT && nmax < kLongSeries;
   const int groups_max = 4;
   const int npw_long = LAT ? long_npw() : groups_max;
