@@ -1100,8 +1100,16 @@ __device__ unsigned long long g_lm_prof[8];
 #define LM_PROF_ADD(k, t0) (void)0
 #endif
 
+// CTAs per SM the register allocation must allow (A/B on sweep / suite16):
+// hidden-1 d <= 2 models are short and numerous -> 6 (80 registers, spills
+// cheaper than the latency they hide); d >= 3 includes the longest series
+// (pathfinder n = 7604), where spills would lengthen the critical chain -> 4
 template <int PM, int D>
-__global__ void __launch_bounds__(128) lm_warp_kernel(LmLaunch L) {
+constexpr int lm_min_blocks() {
+  return PM > 8 ? 4 : (D == 1 || D == 2) ? 6 : 4;  // PM = 32: 3-warp CTAs, 4 per SM (shared memory)
+}
+template <int PM, int D>
+__global__ void __launch_bounds__(PM > 8 ? 96 : 128, lm_min_blocks<PM, D>()) lm_warp_kernel(LmLaunch L) {
   extern __shared__ __align__(16) unsigned char lm_smem[];
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
   const int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + wi;
