@@ -525,10 +525,15 @@ __device__ __forceinline__ void load_x(double (&x)[D], const double* X, int64_t 
   for (int k = 0; k < D; ++k) x[k] = __ldg(X + i * xs + k);
 }
 
-template <int PM, int D>
+// Per-sample passes take a sample split (sw of NW warps sharing one model;
+// NW = 1: the warp owns the model and the lane's sample order is i = lane,
+// lane + 32, ...).  They return / store warp-level sums; NW > 1 callers
+// reduce across warps.
+template <int PM, int D, int NW = 1>
 __device__ double w_energy(const WarpLm<PM>& S, const double* wv, const double* X, const double* Y,
-                           int n, int d, int h, int xs, int lane) {
+                           int n, int d, int h, int xs, int lane, int sw = 0) {
   double acc = 0.0;
+  constexpr int ST = 32 * NW;
   if constexpr (D > 0) {
     H1<D> m;
     m.load(wv);
@@ -536,13 +541,13 @@ __device__ double w_energy(const WarpLm<PM>& S, const double* wv, const double* 
     // then independent exp/div chains (ILP); the accumulation order stays the
     // sample order of the lane
     constexpr int U8 = 8;
-    int i = lane;
-    for (; i + 32 * (U8 - 1) < n; i += 32 * U8) {
+    int i = sw * 32 + lane;
+    for (; i + ST * (U8 - 1) < n; i += ST * U8) {
       double xv[U8][D], yv[U8], r[U8];
 #pragma unroll
       for (int u = 0; u < U8; ++u) {
-        load_x<D>(xv[u], X, i + 32 * u, xs);
-        yv[u] = __ldg(Y + i + 32 * u);
+        load_x<D>(xv[u], X, i + ST * u, xs);
+        yv[u] = __ldg(Y + i + ST * u);
       }
 #pragma unroll
       for (int u = 0; u < U8; ++u) {
@@ -552,7 +557,7 @@ __device__ double w_energy(const WarpLm<PM>& S, const double* wv, const double* 
 #pragma unroll
       for (int u = 0; u < U8; ++u) acc = fma(r[u], r[u], acc);
     }
-    for (; i < n; i += 32) {
+    for (; i < n; i += ST) {
       double x[D];
       load_x<D>(x, X, i, xs);
       double a;
@@ -658,9 +663,9 @@ __device__ void w_stats_blocked(WarpLm<PM>& S, const double* X, const double* Y,
   __syncwarp();
 }
 
-template <int PM, int D>
+template <int PM, int D, int NW = 1>
 __device__ void w_stats(WarpLm<PM>& S, const double* X, const double* Y, int n, int d, int h, int P,
-                        int xs, int lane) {
+                        int xs, int lane, int sw = 0, double* red = nullptr) {
   constexpr int LD = WarpLm<PM>::LD;
   if constexpr (D > 0) {
     constexpr int PP = D + 3;
@@ -692,21 +697,31 @@ __device__ void w_stats(WarpLm<PM>& S, const double* X, const double* Y, int n, 
       for (int p = 0; p < PP; ++p, ++e) acc[e] = fma(jr[p], r, acc[e]);
     };
     constexpr int UB = 4;
-    int i = lane;
-    for (; i + 32 * (UB - 1) < n; i += 32 * UB) {
+    constexpr int ST = 32 * NW;
+    int i = sw * 32 + lane;
+    for (; i + ST * (UB - 1) < n; i += ST * UB) {
       double xv[UB][D], yv[UB];
 #pragma unroll
       for (int u = 0; u < UB; ++u) {
-        load_x<D>(xv[u], X, i + 32 * u, xs);
-        yv[u] = __ldg(Y + i + 32 * u);
+        load_x<D>(xv[u], X, i + ST * u, xs);
+        yv[u] = __ldg(Y + i + ST * u);
       }
 #pragma unroll
       for (int u = 0; u < UB; ++u) sample(xv[u], yv[u]);
     }
-    for (; i < n; i += 32) {
+    for (; i < n; i += ST) {
       double x[D];
       load_x<D>(x, X, i, xs);
       sample(x, __ldg(Y + i));
+    }
+    if constexpr (NW > 1) {  // warp partials -> red[sw][e]; the caller reduces
+      int e = 0;
+#pragma unroll
+      for (int p = 0; p < NA; ++p, ++e) {
+        const double v = warp_sum(acc[e]);
+        if (lane == 0) red[sw * NA + e] = v;
+      }
+      return;
     }
     int e = 0;
 #pragma unroll
@@ -1108,13 +1123,22 @@ template <int PM, int D>
 constexpr int lm_min_blocks() {
   return PM > 8 ? 4 : (D == 1 || D == 2) ? 6 : 4;  // PM = 32: 3-warp CTAs, 4 per SM (shared memory)
 }
-template <int PM, int D>
-__global__ void __launch_bounds__(PM > 8 ? 96 : 128, lm_min_blocks<PM, D>()) lm_warp_kernel(LmLaunch L) {
+// NW = 1: one model per warp.  NW > 1 (hidden-1 long series): one model per
+// CTA of NW warps -- the per-sample passes (objective, J'J / J'r) are split
+// over the warps and reduced in warp order through shared memory; the
+// damped solve and the eigen-solve run on warp 0; the scalar LM / evidence
+// bookkeeping is computed identically by every warp.
+template <int PM, int D, int NW = 1>
+__global__ void __launch_bounds__(NW > 1 ? 32 * NW : (PM > 8 ? 96 : 128),
+                                  NW > 1 ? 1 : lm_min_blocks<PM, D>()) lm_warp_kernel(LmLaunch L) {
   extern __shared__ __align__(16) unsigned char lm_smem[];
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  const int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + wi;
+  const int64_t task = NW > 1 ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * (blockDim.x >> 5) + wi;
   if (task >= L.n_tasks) return;
-  WarpLm<PM>& S = ((WarpLm<PM>*)lm_smem)[wi];
+  WarpLm<PM>& S = NW > 1 ? *(WarpLm<PM>*)lm_smem : ((WarpLm<PM>*)lm_smem)[wi];
+  // NW > 1: cross-warp partials + broadcast slots after the model workspace
+  double* red = (double*)(lm_smem + sizeof(WarpLm<PM>));
+  const bool lead = NW == 1 || wi == 0;
   const bbml_lm_task tk = L.tasks[task];
   const int orig = L.orig_index[task];
   const int n = tk.n, d = tk.d, h = tk.h;
@@ -1122,8 +1146,63 @@ __global__ void __launch_bounds__(PM > 8 ? 96 : 128, lm_min_blocks<PM, D>()) lm_
   const int xs = L.x_stride;
   const double* X = L.X + tk.row_begin * (int64_t)xs;
   const double* Y = L.y + tk.row_begin;
+  const double* X_ = X;
+  const double* Y_ = Y;
+  const int n_ = n, d_ = d, h_ = h, xs_ = xs;
+  const int sw = NW > 1 ? wi : 0;
+  auto sync = [&]() {
+    if constexpr (NW > 1) __syncthreads();
+    else __syncwarp();
+  };
+  // objective over all samples (NW > 1: warp partials summed in warp order)
+  auto energy = [&](const double* wv) -> double {
+    const double v = w_energy<PM, D, NW>(S, wv, X_, Y_, n_, d_, h_, xs_, lane, sw);
+    if constexpr (NW == 1) {
+      return v;
+    } else {
+      __syncthreads();
+      if (lane == 0) red[wi] = v;
+      __syncthreads();
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) t += red[w];
+      return t;
+    }
+  };
+  auto stats = [&]() {
+    if constexpr (NW == 1) {
+      w_stats<PM, D>(S, X, Y, n, d, h, P, xs, lane);
+    } else {
+      constexpr int PP = D + 3;
+      constexpr int NA = PP * (PP + 1) / 2 + PP;
+      __syncthreads();
+      w_stats<PM, D, NW>(S, X, Y, n, d, h, P, xs, lane, sw, red);
+      __syncthreads();
+      if (wi == 0) {
+        constexpr int LD = WarpLm<PM>::LD;
+        for (int e = lane; e < NA; e += 32) {
+          double v = 0.0;
+#pragma unroll
+          for (int w = 0; w < NW; ++w) v += red[w * NA + e];
+          int a = 0, b = e;  // e -> (a, b) in the upper-triangle order, then J'r
+          if (e < PP * (PP + 1) / 2) {
+            while (b >= PP - a) {
+              b -= PP - a;
+              ++a;
+            }
+            b += a;
+            S.jtj[a * LD + b] = v;
+            S.jtj[b * LD + a] = v;
+          } else {
+            S.jtr[e - PP * (PP + 1) / 2] = v;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  };
 
-  if (lane == 0) {  // init (brbpnn.py:323-331)
+  if (lead && lane == 0) {  // init (brbpnn.py:323-331)
     Pcg64 rng;
     rng.seed(tk.seed);
     const double s1 = __ddiv_rn(1.0, __dsqrt_rn((double)d));
@@ -1144,12 +1223,12 @@ __global__ void __launch_bounds__(PM > 8 ? 96 : 128, lm_min_blocks<PM, D>()) lm_
         }
     }
   }
-  __syncwarp();
+  sync();
 
   double alpha = tk.alpha0, beta = tk.beta0, mu = tk.mu0;
   const bool est = tk.estimate != 0;
   double* hist = (tk.hist_offset >= 0) ? L.history + tk.hist_offset : nullptr;
-  double e_d = w_energy<PM, D>(S, S.w, X, Y, n, d, h, xs, lane);
+  double e_d = energy(S.w);
   double e_w = 0.0;
   for (int i = 0; i < P; ++i) e_w = fma(S.w[i], S.w[i], e_w);
   bool have_stats = false;
@@ -1161,7 +1240,7 @@ __global__ void __launch_bounds__(PM > 8 ? 96 : 128, lm_min_blocks<PM, D>()) lm_
   for (int ep = 0; ep < tk.max_epochs; ++ep) {
     if (!have_stats) {
       LM_PROF_T(t0);
-      w_stats<PM, D>(S, X, Y, n, d, h, P, xs, lane);
+      stats();
       LM_PROF_ADD(0, t0);
     }
     const double f0 = __dadd_rn(__dmul_rn(beta, e_d), __dmul_rn(alpha, e_w));
@@ -1170,18 +1249,26 @@ __global__ void __launch_bounds__(PM > 8 ? 96 : 128, lm_min_blocks<PM, D>()) lm_
     while (true) {
       ++trials;
       LM_PROF_T(t2);
-      const bool solved = PM > 8 ? w_solve_cols<PM>(S, P, alpha, beta, mu, lane)
-                                 : w_solve<PM>(S, P, alpha, beta, mu, lane);
+      bool solved = true;
+      if (lead) {
+        solved = PM > 8 ? w_solve_cols<PM>(S, P, alpha, beta, mu, lane)
+                        : w_solve<PM>(S, P, alpha, beta, mu, lane);
+        if (lane < P) S.wt[lane] = __dadd_rn(S.w[lane], S.delta[lane]);
+      }
+      if constexpr (NW > 1) {
+        if (wi == 0 && lane == 0) red[NW * 64] = solved ? 1.0 : 0.0;
+        __syncthreads();
+        solved = red[NW * 64] != 0.0;
+      }
       LM_PROF_ADD(2, t2);
       if (!solved) {
         code = BBML_MODEL_SINGULAR;
         fail_mu = mu;
         break;
       }
-      if (lane < P) S.wt[lane] = __dadd_rn(S.w[lane], S.delta[lane]);
-      __syncwarp();
+      sync();
       LM_PROF_T(t3);
-      td = w_energy<PM, D>(S, S.wt, X, Y, n, d, h, xs, lane);
+      td = energy(S.wt);
       LM_PROF_ADD(3, t3);
       tw = 0.0;
       for (int i = 0; i < P; ++i) tw = fma(S.wt[i], S.wt[i], tw);
@@ -1195,8 +1282,8 @@ __global__ void __launch_bounds__(PM > 8 ? 96 : 128, lm_min_blocks<PM, D>()) lm_
       if (mu > tk.mu_max) break;
     }
     if (code != BBML_MODEL_OK || !accepted) break;
-    if (lane < P) S.w[lane] = S.wt[lane];
-    __syncwarp();
+    if (lead && lane < P) S.w[lane] = S.wt[lane];
+    sync();
     e_d = td;
     e_w = tw;
     const double f1 = __dadd_rn(__dmul_rn(beta, e_d), __dmul_rn(alpha, e_w));
@@ -1204,15 +1291,23 @@ __global__ void __launch_bounds__(PM > 8 ? 96 : 128, lm_min_blocks<PM, D>()) lm_
     int pinned = 0;
     if (est) {
       LM_PROF_T(t0);
-      w_stats<PM, D>(S, X, Y, n, d, h, P, xs, lane);
+      stats();
       LM_PROF_ADD(0, t0);
       have_stats = true;
       LM_PROF_T(t1);
       // P <= 5: cyclic Jacobi (converges in a few sweeps at this size);
       // P >= 6: Householder + bisection
-      if constexpr (WarpLm<PM>::kWide) gamma = w_gamma_tri<PM>(S, P, alpha, beta, lane);
-      else if (P >= 6) gamma = w_gamma_tri<PM>(S, P, alpha, beta, lane);
-      else gamma = w_gamma<PM>(S, P, alpha, beta, lane);
+      if (lead) {
+        if constexpr (WarpLm<PM>::kWide) gamma = w_gamma_tri<PM>(S, P, alpha, beta, lane);
+        else if (P >= 6) gamma = w_gamma_tri<PM>(S, P, alpha, beta, lane);
+        else gamma = w_gamma<PM>(S, P, alpha, beta, lane);
+      }
+      if constexpr (NW > 1) {
+        if (wi == 0 && lane == 0) red[NW * 64 + 1] = gamma;
+        __syncthreads();
+        gamma = red[NW * 64 + 1];
+        __syncthreads();
+      }
       LM_PROF_ADD(1, t1);
       double na, nb;
       if (e_w > 0.0) {
@@ -1236,7 +1331,7 @@ __global__ void __launch_bounds__(PM > 8 ? 96 : 128, lm_min_blocks<PM, D>()) lm_
     last_mu = mu;
     last_gamma = gamma;
     epochs = ep + 1;
-    if (hist && lane == 0) {
+    if (hist && lead && lane == 0) {
       double* r = hist + (int64_t)ep * 10;
       r[0] = ep; r[1] = f0; r[2] = f1; r[3] = e_d; r[4] = e_w;
       r[5] = alpha; r[6] = beta; r[7] = gamma; r[8] = mu; r[9] = pinned;
@@ -1256,7 +1351,8 @@ __global__ void __launch_bounds__(PM > 8 ? 96 : 128, lm_min_blocks<PM, D>()) lm_
     prev_w = e_w;
     have_prev = true;
   }
-  __syncwarp();
+  sync();
+  if (!lead) return;
   double* W = L.weights + tk.w_offset;
   if (lane < P) W[lane] = S.w[lane];
   if (lane == 0) {
@@ -1287,11 +1383,22 @@ static cudaError_t lm_launch_warp(const LmLaunch& L, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// launch key: 1..4 = hidden-1 warp fast path with d inputs; 8 / 32 = warp
+// hidden-1 long series: one model per CTA of LM_NW warps
+constexpr int LM_NW = 4;
+constexpr int kLongLm = 2048;  // samples from which a hidden-1 fit gets a CTA
+template <int D>
+static cudaError_t lm_launch_multi(const LmLaunch& L, cudaStream_t s) {
+  const size_t smem = sizeof(WarpLm<8>) + (size_t)(LM_NW * 64 + 8) * sizeof(double);
+  lm_warp_kernel<8, D, LM_NW><<<L.n_tasks, 32 * LM_NW, smem, s>>>(L);
+  return cudaGetLastError();
+}
+
+// launch key: 1..4 = hidden-1 warp fast path with d inputs (101..104: the
+// same for n >= kLongLm, one CTA of LM_NW warps per model); 8 / 32 = warp
 // kernels (P <= 8 / P <= 32); 512 = wide CTA-per-model kernel (lm_wide.cu)
 static int lm_key(const bbml_lm_task& t) {
   const int P = t.h * (t.d + 2) + 1;
-  if (t.h == 1 && t.d <= 4) return t.d;
+  if (t.h == 1 && t.d <= 4) return t.n >= kLongLm ? 100 + t.d : t.d;
   return P <= 8 ? 8 : P <= 32 ? 32 : 512;
 }
 
@@ -1384,7 +1491,11 @@ bbml_status lm_train_launch(const bbml_lm_task* tasks, int32_t n_tasks, const do
     L.history = history;
     L.status = status;
     cudaError_t e;
-    if (b == 1) e = lm_launch_warp<8, 1>(L, cs);
+    if (b == 101) e = lm_launch_multi<1>(L, cs);
+    else if (b == 102) e = lm_launch_multi<2>(L, cs);
+    else if (b == 103) e = lm_launch_multi<3>(L, cs);
+    else if (b == 104) e = lm_launch_multi<4>(L, cs);
+    else if (b == 1) e = lm_launch_warp<8, 1>(L, cs);
     else if (b == 2) e = lm_launch_warp<8, 2>(L, cs);
     else if (b == 3) e = lm_launch_warp<8, 3>(L, cs);
     else if (b == 4) e = lm_launch_warp<8, 4>(L, cs);

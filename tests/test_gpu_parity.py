@@ -331,3 +331,28 @@ def test_br_wide_accuracy_parity_hidden64():
     acc_ora = 100 * (1 - float(np.mean(ora)))
     print("hidden-64 accuracy device %.3f oracle %.3f" % (acc_dev, acc_ora))
     assert abs(acc_dev - acc_ora) <= 0.5
+
+
+def test_br_hidden1_long_series_multiwarp():
+    """Hidden-1 fits with n >= 2048 training rows run one model per CTA of 4
+    warps (sample passes split over warps, reduced in warp order); against
+    the oracle's train_one on the same random split: predictions <= 1e-6
+    relative (accuracy gate for a beta-clamped degenerate fit, as in
+    test_train_one_matches_reference_golden)."""
+    from paper_2202_07798_b200 import synth
+    from paper_2202_07798_b200.experiment import ExperimentConfig, train_many
+    from paper_2202_07798_b200.traces import BbSeries, SplitMode
+
+    raw = synth.app20(axis=tuple(range(1, 65)))[:4]
+    series = [BbSeries(k, X, y) for k, X, y in raw]
+    cfg = ExperimentConfig(split_mode=SplitMode.RANDOM, seed=1, br_max_epochs=300,
+                           models=("brbpnn",))
+    res = train_many([(s, "brbpnn") for s in series], cfg).results
+    for (k, X, y), r in zip(raw, res):
+        o = O.train_one(k, X, y, "brbpnn", mode="random", base_seed=1, br_max_epochs=300)
+        assert r.error is None and o.error is None, (k, r.error, o.error)
+        assert r.n_train == o.n_train and r.n_train >= 2048
+        floor = 1e-6 * max(1.0, float(np.max(np.abs(y))))
+        if abs(r.mse - o.mse) <= 1e-12 or _rel(r.pred_raw, o.pred_raw, floor) <= 1e-6:
+            continue
+        assert abs(r.mse - o.mse) <= 0.005, (k, r.mse, o.mse)
