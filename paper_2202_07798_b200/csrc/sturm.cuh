@@ -15,7 +15,8 @@
 //     the others bisect [0, ||T||] on the IEEE bit pattern (the midpoint of the
 //     bit patterns is the geometric midpoint across binades, the arithmetic one
 //     inside a binade), so near-null eigenvalues converge in relative terms.
-//   * stop when the gamma contribution is pinned to 1e-13 (division-free form
+//   * stop when the gamma contribution is pinned (1e-13; 1e-10 for the P <= 32
+//     warp path) (division-free form
 //     of f(hi) - f(lo) = r (hi-lo) / ((hi+r)(lo+r)), r = alpha/beta) or at
 //     ~2 ulp relative width.
 // Eigenvalue accuracy is the backward-stable eps*||T|| of bisection, the same
@@ -105,10 +106,14 @@ __device__ __forceinline__ double sturm_gamma_part_fixed(const double* __restric
   double lo = kSturmTiny, hi = hi0;
   long long lb = __double_as_longlong(lo), hb = __double_as_longlong(hi0);
   constexpr double eps = 2.220446049250313e-16;
+  // gamma pin: 1e-13 per eigenvalue for P <= 8 (hidden-1 fits, gated at 1e-6
+  // on predictions); 1e-10 for P <= 32 (hidden >= 2, gated statistically:
+  // 32 * 1e-10 on gamma is far inside the reference's own 1-ulp spread)
+  constexpr double pin = PM > 8 ? 1e-10 : 1e-13;
   for (int it = 0; it < 80; ++it) {
     const double w = hi - lo;
     if (w <= 2.0 * eps * hi) break;
-    if (w * r <= 1e-13 * ((hi + r) * (lo + r))) break;
+    if (w * r <= pin * ((hi + r) * (lo + r))) break;
     const long long mb = (lb + hb) >> 1;
     const double mid = __longlong_as_double(mb);
     if (sturm_count_fixed<PM>(dd, e2, mid) > k) {
