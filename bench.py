@@ -383,6 +383,16 @@ def main():
             rl["lm"] = {"bound": "fp64-pipe", "kernel": f"{kn} (bbml_lm_train)",
                         "achieved": a, "peak": peak64, "unit": "TFLOP/s", "frac": a / peak64,
                         "kernel_ms": lm_ms, "algorithmic_flops": lm_fl, "traffic": None}
+        try:  # DRAM bytes per launch of the dominant kernel from the committed ncu capture
+            with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+                traffic = json.load(fh)
+        except (OSError, ValueError):
+            traffic = {}
+        for v in rl.values():
+            name = v["kernel"].split(" ")[0]
+            if name in traffic:
+                v["traffic"] = traffic[name]["bytes_per_launch"]
+                v["traffic_source"] = f'{traffic[name]["report"]} ({traffic[name]["launch"]})'
         dom = max(rl, key=lambda k: rl[k]["kernel_ms"]) if rl else None
         roof = dict(rl[dom]) if dom else {}
         roof["peak_source"] = ("measured: bbml_fma_peak FMA-pipe microbenchmark on this GPU "
