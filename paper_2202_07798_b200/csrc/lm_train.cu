@@ -1,5 +1,9 @@
 // lm_train.cu — batched Bayesian-regularised Levenberg-Marquardt trainer
-// (BR-BPNN), one model per CTA, all state FP64 in shared memory.
+// (BR-BPNN), all state FP64.  Training kernels: one model per warp
+// (`lm_warp_kernel<PM, D>`, P <= 8 / P <= 32, workspace in shared memory),
+// one model per CTA of 4 warps for hidden-1 series with n >= 2048, and the
+// wide CTA-per-model kernel in lm_wide.cu (P <= 512).  The CTA helpers at the
+// top (LmSmem, damped_solve, jacobi_gamma) serve the unit-level entry points.
 //
 // Reference semantics (bbcount/brbpnn.py):
 //   tansig 33-38, forward 85-91, pack/unpack 94-106, objective 109-115,
@@ -10,12 +14,9 @@
 //   J'J clipped at 0, gamma = sum beta*l/(beta*l+alpha) with the OLD alpha,beta,
 //   pinned clamps), train 286-346 (records, early stop after 5 stable epochs).
 //
-// Per epoch the kernel forms J'J and J'r ONCE at the accepted weights and
-// reuses them for (a) the evidence update and (b) every LM trial of the next
-// epoch (the reference recomputes the identical J at the same w each trial).
-// J rows are staged CH at a time in shared memory and contracted into the
-// upper triangle; LU + triangular solves and a parallel cyclic Jacobi
-// eigen-solver run in shared memory.
+// Per epoch a model forms J'J and J'r ONCE at the accepted weights and reuses
+// them for (a) the evidence update and (b) every LM trial of the next epoch
+// (the reference recomputes the identical J at the same w each trial).
 #include <algorithm>
 #include <cstdio>
 #include <vector>
@@ -79,64 +80,6 @@ __device__ __forceinline__ double br_sample(const double* __restrict__ w, const 
   }
   if (jrow) jrow[hd + 2 * h] = 1.0;
   return __dadd_rn(out, w[hd + 2 * h]);
-}
-
-// E_D = sum r^2 at weights wv (objective, brbpnn.py:109-115)
-__device__ double energy_pass(const double* wv, const double* X, const double* Y, int n, int d,
-                              int h, int xs, double* red) {
-  double acc = 0.0;
-  double x[BBML_MAX_INPUTS];
-  for (int i = threadIdx.x; i < n; i += LM_NT) {
-    for (int k = 0; k < d; ++k) x[k] = __ldg(X + (int64_t)i * xs + k);
-    const double r = __dsub_rn(br_sample(wv, x, d, h, nullptr), __ldg(Y + i));
-    acc = fma(r, r, acc);
-  }
-  return block_sum(acc, red);
-}
-
-// J'J (full) and J'r at weights S.w
-template <int CH>
-__device__ void stats_pass(LmSmem& S, const double* X, const double* Y, int n, int d, int h, int P,
-                           int xs) {
-  const int npair = P * (P + 1) / 2;
-  for (int e = threadIdx.x; e < P * P; e += LM_NT) S.jtj[e] = 0.0;
-  for (int e = threadIdx.x; e < P; e += LM_NT) S.jtr[e] = 0.0;
-  __syncthreads();
-  double x[BBML_MAX_INPUTS];
-  for (int base = 0; base < n; base += CH) {
-    const int cnt = min(CH, n - base);
-    for (int c = threadIdx.x; c < cnt; c += LM_NT) {
-      const int i = base + c;
-      for (int k = 0; k < d; ++k) x[k] = __ldg(X + (int64_t)i * xs + k);
-      S.rc[c] = __dsub_rn(br_sample(S.w, x, d, h, S.Jc + c * P), __ldg(Y + i));
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < npair + P; e += LM_NT) {
-      if (e < npair) {
-        // e -> (a, b) with a <= b, row-major upper triangle
-        int a = 0, rem = e;
-        while (rem >= P - a) {
-          rem -= P - a;
-          ++a;
-        }
-        const int b = a + rem;
-        double s = S.jtj[a * P + b];
-        for (int c = 0; c < cnt; ++c) s = fma(S.Jc[c * P + a], S.Jc[c * P + b], s);
-        S.jtj[a * P + b] = s;
-      } else {
-        const int a = e - npair;
-        double s = S.jtr[a];
-        for (int c = 0; c < cnt; ++c) s = fma(S.Jc[c * P + a], S.rc[c], s);
-        S.jtr[a] = s;
-      }
-    }
-    __syncthreads();
-  }
-  for (int e = threadIdx.x; e < P * P; e += LM_NT) {
-    const int a = e / P, b = e % P;
-    if (a > b) S.jtj[e] = S.jtj[b * P + a];
-  }
-  __syncthreads();
 }
 
 // delta = solve(beta J'J + (mu+alpha) I, -(beta J'r + alpha w)); returns false on a zero pivot
@@ -305,160 +248,6 @@ __device__ double jacobi_gamma(LmSmem& S, int P, double alpha, double beta, doub
   return g;
 }
 
-template <int PMAX, int CH>
-__global__ void __launch_bounds__(LM_NT) lm_train_kernel(LmLaunch L) {
-  const int task = blockIdx.x;
-  if (task >= L.n_tasks) return;
-  const bbml_lm_task tk = L.tasks[task];
-  const int orig = L.orig_index[task];
-  const int n = tk.n, d = tk.d, h = tk.h;
-  const int P = h * (d + 2) + 1;
-  const int xs = L.x_stride;
-  const double* X = L.X + tk.row_begin * (int64_t)xs;
-  const double* Y = L.y + tk.row_begin;
-
-  extern __shared__ double sm[];
-  LmSmem S;
-  double* q = sm;
-  S.w = q; q += PMAX;
-  S.wt = q; q += PMAX;
-  S.delta = q; q += PMAX;
-  S.jtr = q; q += PMAX;
-  S.rhs = q; q += PMAX;
-  S.jtj = q; q += PMAX * PMAX;
-  S.A = q; q += PMAX * PMAX;
-  S.Jc = q; q += CH * PMAX;
-  S.rc = q; q += (CH > LM_NT ? CH : LM_NT);
-  S.cs = q; q += 2 * (PMAX + 2);
-  S.red = q; q += LM_WARPS + 2;
-  S.piv = (int*)q; q += (PMAX + 1) / 2 + 1;
-  S.flag = (int*)q;
-
-  // init (brbpnn.py:323-331): thread 0 draws P uniforms in pack order
-  if (threadIdx.x == 0) {
-    Pcg64 rng;
-    rng.seed(tk.seed);
-    const double s1 = __ddiv_rn(1.0, __dsqrt_rn((double)d));
-    const double s2 = __ddiv_rn(1.0, __dsqrt_rn((double)h));
-    const int hd = h * d;
-    for (int i = 0; i < hd + h; ++i) S.w[i] = rng.uniform(-s1, s1);
-    for (int i = hd + h; i < P; ++i) S.w[i] = rng.uniform(-s2, s2);
-  }
-  __syncthreads();
-
-  double alpha = tk.alpha0, beta = tk.beta0, mu = tk.mu0;
-  const bool est = tk.estimate != 0;
-  double* hist = (tk.hist_offset >= 0) ? L.history + tk.hist_offset : nullptr;
-
-  double e_d = energy_pass(S.w, X, Y, n, d, h, xs, S.red);
-  double e_w = 0.0;
-  for (int i = 0; i < P; ++i) e_w = fma(S.w[i], S.w[i], e_w);
-  bool have_stats = false;
-  int code = BBML_MODEL_OK, trials = 0, epochs = 0, any_pinned = 0;
-  double fail_mu = 0.0, last_mu = NAN, last_gamma = NAN;
-  double prev_g = 0.0, prev_d = 0.0, prev_w = 0.0;
-  bool have_prev = false;
-  int stable = 0;
-
-  for (int ep = 0; ep < tk.max_epochs; ++ep) {
-    if (!have_stats) stats_pass<CH>(S, X, Y, n, d, h, P, xs);
-    const double f0 = __dadd_rn(__dmul_rn(beta, e_d), __dmul_rn(alpha, e_w));
-    bool accepted = false;
-    double td = 0.0, tw = 0.0;
-    while (true) {
-      ++trials;
-      if (!damped_solve(S, P, alpha, beta, mu)) {
-        code = BBML_MODEL_SINGULAR;
-        fail_mu = mu;
-        break;
-      }
-      for (int i = threadIdx.x; i < P; i += LM_NT) S.wt[i] = __dadd_rn(S.w[i], S.delta[i]);
-      __syncthreads();
-      td = energy_pass(S.wt, X, Y, n, d, h, xs, S.red);
-      tw = 0.0;
-      for (int i = 0; i < P; ++i) tw = fma(S.wt[i], S.wt[i], tw);
-      const double f1 = __dadd_rn(__dmul_rn(beta, td), __dmul_rn(alpha, tw));
-      if (f1 < f0) {
-        mu = fmax(__dmul_rn(mu, tk.mu_dec), 1e-20);
-        accepted = true;
-        break;
-      }
-      mu = __dmul_rn(mu, tk.mu_inc);
-      if (mu > tk.mu_max) break;
-    }
-    if (code != BBML_MODEL_OK || !accepted) break;
-    __syncthreads();
-    for (int i = threadIdx.x; i < P; i += LM_NT) S.w[i] = S.wt[i];
-    __syncthreads();
-    e_d = td;
-    e_w = tw;
-    const double f1 = __dadd_rn(__dmul_rn(beta, e_d), __dmul_rn(alpha, e_w));
-    double gamma = NAN;
-    int pinned = 0;
-    if (est) {
-      stats_pass<CH>(S, X, Y, n, d, h, P, xs);
-      have_stats = true;
-      gamma = jacobi_gamma(S, P, alpha, beta, nullptr);
-      double na, nb;
-      if (e_w > 0.0) {
-        na = __ddiv_rn(gamma, __dmul_rn(2.0, e_w));
-      } else {
-        na = 1e12;
-        pinned = 1;
-      }
-      if (e_d > 0.0) {
-        nb = __ddiv_rn(__dsub_rn((double)n, gamma), __dmul_rn(2.0, e_d));
-      } else {
-        nb = 1e12;
-        pinned = 1;
-      }
-      alpha = fmin(fmax(na, 1e-12), 1e12);
-      beta = fmin(fmax(nb, 1e-12), 1e12);
-    } else {
-      have_stats = false;
-    }
-    any_pinned |= pinned;
-    last_mu = mu;
-    last_gamma = gamma;
-    epochs = ep + 1;
-    if (hist && threadIdx.x == 0) {
-      double* r = hist + (int64_t)ep * 10;
-      r[0] = ep; r[1] = f0; r[2] = f1; r[3] = e_d; r[4] = e_w;
-      r[5] = alpha; r[6] = beta; r[7] = gamma; r[8] = mu; r[9] = pinned;
-    }
-    if (have_prev && est) {
-      const bool ok = fabs(gamma - prev_g) <= 1e-7 * fmax(fabs(prev_g), 1e-300) &&
-                      fabs(e_d - prev_d) <= 1e-7 * fmax(fabs(prev_d), 1e-300) &&
-                      fabs(e_w - prev_w) <= 1e-7 * fmax(fabs(prev_w), 1e-300);
-      if (ok) {
-        if (++stable >= 5) break;
-      } else {
-        stable = 0;
-      }
-    }
-    prev_g = gamma;
-    prev_d = e_d;
-    prev_w = e_w;
-    have_prev = true;
-  }
-
-  __syncthreads();
-  double* W = L.weights + tk.w_offset;
-  for (int i = threadIdx.x; i < P; i += LM_NT) W[i] = S.w[i];
-  if (threadIdx.x == 0) {
-    bbml_model_status st{};
-    st.code = code;
-    st.epochs = epochs;
-    st.detail = any_pinned;
-    st.trials = trials;
-    st.value = fail_mu;
-    st.mu = last_mu;
-    st.gamma = last_gamma;
-    st.alpha = alpha;
-    st.beta = beta;
-    L.status[orig] = st;
-  }
-}
 
 // ===========================================================================
 // Warp-per-model LM trainer for P <= 32 (all hidden-1 models, and hidden 10
