@@ -4,10 +4,12 @@
                     [--restarts R] [--precision 32|64] [--impl ours|reference]
 
 One step = train every model of the workload from scratch (PNN and BR-BPNN,
-one fused kernel each, concurrently) and predict every model's test rows.
+one fused kernel each, concurrently), predict every model's test rows and
+compute every model's test MSE / Pearson / Spearman on the device.
 Inputs (CSR-packed, normalised training/test rows) are resident in HBM for
 `value`; `e2e` times the public batched call (batch.fit_predict path) with
-H2D from pinned host buffers and D2H of weights/status/predictions each step.
+H2D from pinned host buffers and D2H of weights / status / per-model test
+metrics (computed on the device from the predictions) each step.
 Multi-GPU (torchrun): every rank trains its own restarts of the workload
 (weak scaling, no data-path collective); time = max over ranks.
 `--impl reference` times the CPU oracle port (numpy restatement of the
@@ -312,16 +314,19 @@ def main():
     step_ms = [e[0].elapsed_time(e[3]) for e in ev]
     total_s = sum(step_ms) / 1e3
 
+    # clock sampling covers the device-timed region; stopped before the e2e loop
+    # (an nvidia-smi query holds the driver and stalls host-side CUDA calls)
+    if clk:
+        clk.terminate()
+        clk.wait()
+
     # end-to-end: public batched call with pinned host inputs, H2D + D2H every step
     e2e_times = []
     for k in range(args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        batch.fit_predict(wl, dev)
+        batch.fit_predict(wl, dev, predictions=False)  # result: weights, status, metrics
         e2e_times.append(time.perf_counter() - t0)
-    if clk:
-        clk.terminate()
-        clk.wait()
 
     # dominant kernel (PNN train) timed alone on its stream for the roofline
     # each training kernel timed alone on its launching stream (CUDA events)
@@ -422,7 +427,9 @@ def main():
                        "br_precision": "fp64", "l2": "flushed (256 MiB write) between steps",
                        "split": spec.mode.value},
             "e2e": {"value": e2e_value, "unit": "models/s", "h2d_bytes_per_step": dev.h2d_bytes,
-                    "d2h_bytes_per_step": dev.d2h_bytes},
+                    "d2h_bytes_per_step": dev.d2h_bytes_for(False),
+                    "result": "trained weights + status + per-model test MSE / Pearson / "
+                              "Spearman (bbml_metrics)"},
             "roofline": roof,
             "gpu_launches": launches,
             "models_failed": n_bad,
@@ -434,6 +441,7 @@ def main():
             "clocks": summarize_clocks(clock_path, local),
             "cpu_baseline": cpu,
             "step_ms": step_ms,
+            "e2e_step_ms": [1e3 * t for t in e2e_times],
         }
         out = json.dumps(line)
         print(out, flush=True)

@@ -10,6 +10,7 @@
  *   bbml_lm_train     <- bbcount/brbpnn.py:286-346   brbpnn.train (+ lm_trial/lm_step 174-211,
  *                                                     solve_damped 153-171, evidence_update 221-251)
  *   bbml_predict      <- bbcount/pnn.py:108-118      pnn.forward
+ *   bbml_metrics      <- bbcount/metrics.py:33-76    mse / pearson / spearman
  *                        bbcount/brbpnn.py:85-91     brbpnn.forward
  *                        bbcount/persist.py:35-43    SavedModel.predict_normalized / predict_counts
  *   bbml_pnn_loss_grad<- bbcount/pnn.py:121-147      pnn.loss_and_grads (unit level)
@@ -142,6 +143,20 @@ bbml_status bbml_lm_train(const bbml_lm_task* tasks, int32_t n_tasks, const doub
 bbml_status bbml_predict(const bbml_pred_task* tasks, int32_t n_tasks, const double* Xq,
                          int32_t x_stride, const double* weights, const double* norm,
                          double* out, void* stream);
+
+/* ---- per-model test metrics ----
+   Replaces the host loop over bbcount/metrics.py mse / pearson / spearman
+   (metrics.py:33-76) as experiment.train_one applies them (experiment.py:128-152).
+   Task i (bbml_pred_task reused): n test rows; actual_norm / actual_raw rows at
+   row_begin; predictions (normalised) at w_offset of pred; norm_offset -> the
+   series' [x_min(d), x_max(d), y_min, y_max] in norm.  Writes 4 doubles at
+   out_offset: mse (normalised space), pearson and spearman of the de-normalised
+   predictions vs actual_raw (NaN = undefined: constant vector or n < 2), and
+   1.0 if Spearman / Pearson were computed on the device (0.0 when n > 4096:
+   the caller computes them). */
+bbml_status bbml_metrics(const bbml_pred_task* tasks, int32_t n_tasks, const double* pred,
+                         const double* actual_norm, const double* actual_raw,
+                         const double* norm, double* out, void* stream);
 
 /* ---- unit-level kernels (one model per task; rows at row_begin, n rows) ---- */
 /* loss[i] and grads (P doubles at w_offset of grads) of the batch NLL */

@@ -40,10 +40,25 @@ class Workload:
     P_lm: np.ndarray
     precision: int = 64
     errors: Optional[dict] = None  # series index -> split error text
+    test_raw_y: Optional[np.ndarray] = None  # raw test counts, packed like test.y
 
     @property
     def n_models(self) -> int:
         return len(self.pnn) + len(self.lm)
+
+    def norm_rows(self) -> np.ndarray:
+        """(series, 2*d_max+2) rows of [x_min(d), x_max(d), y_min, y_max]."""
+        dmax = max([int(self.train.d.max()) if len(self.train.d) else 1, 1])
+        rows = np.zeros((len(self.keys), 2 * dmax + 2))
+        for i, nm in enumerate(self.norms):
+            if nm is None:
+                continue
+            d = len(nm.x_min)
+            rows[i, :d] = nm.x_min
+            rows[i, d:2 * d] = nm.x_max
+            rows[i, 2 * d] = nm.y_min
+            rows[i, 2 * d + 1] = nm.y_max
+        return rows
 
     def pred_tasks(self) -> np.ndarray:
         """Predict table over all models (PNN first), test rows of each model's series,
@@ -71,7 +86,7 @@ def build_workload(series: Sequence[BbSeries], spec: SplitSpec, *, kinds=("pnn",
     """Split + normalise every series once (traces.py semantics), then one
     PNN and/or BR task per (series, restart); restart r seeds the model with
     experiment.series_seed(r, key, kind)."""
-    keys, norms, Xtr, ytr, Xte, yte, errors = [], [], [], [], [], [], {}
+    keys, norms, Xtr, ytr, Xte, yte, errors, yraw = [], [], [], [], [], [], {}, []
     for s in series:
         try:
             tr, te = split(s, spec)
@@ -83,6 +98,7 @@ def build_workload(series: Sequence[BbSeries], spec: SplitSpec, *, kinds=("pnn",
                 lst.append(np.zeros((0, s.arity)))
             ytr.append(np.zeros(0))
             yte.append(np.zeros(0))
+            yraw.append(np.zeros(0))
             continue
         nm = fit_normalizer(tr)
         keys.append(s.key)
@@ -91,6 +107,7 @@ def build_workload(series: Sequence[BbSeries], spec: SplitSpec, *, kinds=("pnn",
         ytr.append(nm.transform_targets(tr.y))
         Xte.append(nm.transform_features(te.X))
         yte.append(nm.transform_targets(te.y))
+        yraw.append(np.asarray(te.y, dtype=np.float64))
     train = engine.pack(Xtr, ytr)
     test = engine.pack(Xte, yte)
     ok = np.array([i for i in range(len(keys)) if i not in errors], dtype=np.int64)
@@ -126,7 +143,8 @@ def build_workload(series: Sequence[BbSeries], spec: SplitSpec, *, kinds=("pnn",
     return Workload(train, test, keys, norms, empty_p if pt is None else pt,
                     empty_l if lt is None else lt, ps, ls,
                     np.zeros(0, np.int64) if pt is None else pP,
-                    np.zeros(0, np.int64) if lt is None else lP, precision, errors)
+                    np.zeros(0, np.int64) if lt is None else lP, precision, errors,
+                    np.concatenate(yraw) if yraw else np.zeros(0))
 
 
 class DeviceWorkload:
@@ -143,6 +161,9 @@ class DeviceWorkload:
         self.X = torch.empty_like(src.X, device=dev)
         self.y = torch.empty_like(src.y, device=dev)
         self.Xq = torch.empty_like(src.Xq, device=dev)
+        self.yq = torch.empty_like(src.yq, device=dev)
+        self.yq_raw = torch.empty_like(src.yq_raw, device=dev)
+        self.norms = torch.empty_like(src.norms, device=dev)
         self.upload()
         self.n_p, self.n_l = len(wl.pnn), len(wl.lm)
         W = int(wl.P_pnn.sum() + wl.P_lm.sum())
@@ -153,15 +174,33 @@ class DeviceWorkload:
         self.side = torch.cuda.Stream(device=dev)
         self.pnn_tab = np.ascontiguousarray(wl.pnn)
         self.lm_tab = np.ascontiguousarray(wl.lm)
+        # per-model test metrics (bbml_metrics): predictions at the predict
+        # table's out_offset, targets at the series' test rows
+        sid = np.concatenate([wl.pnn_series, wl.lm_series]).astype(np.int64)
+        width = wl.norm_rows().shape[1]
+        mt = np.zeros(wl.n_models, dtype=PRED_TASK)
+        mt["row_begin"] = wl.test.row_begin[sid] if len(sid) else 0
+        mt["n"] = self.pred_tab["n"]
+        mt["w_offset"] = self.pred_tab["out_offset"]
+        mt["d"] = self.pred_tab["d"]
+        mt["h"] = 1
+        mt["norm_offset"] = sid * width
+        mt["out_offset"] = np.arange(wl.n_models, dtype=np.int64) * 4
+        self.met_tab = mt
+        self.metrics = torch.empty(max(4 * wl.n_models, 1), dtype=torch.float64, device=dev)
+
+    def _inputs(self):
+        return (("X", self.X, self.host.X), ("y", self.y, self.host.y), ("Xq", self.Xq, self.host.Xq),
+                ("yq", self.yq, self.host.yq), ("yq_raw", self.yq_raw, self.host.yq_raw),
+                ("norms", self.norms, self.host.norms))
 
     def upload(self):
-        self.X.copy_(self.host.X, non_blocking=True)
-        self.y.copy_(self.host.y, non_blocking=True)
-        self.Xq.copy_(self.host.Xq, non_blocking=True)
+        for _, dst, src in self._inputs():
+            dst.copy_(src, non_blocking=True)
 
     @property
     def h2d_bytes(self) -> int:
-        return sum(t.numel() * t.element_size() for t in (self.host.X, self.host.y, self.host.Xq))
+        return sum(src.numel() * src.element_size() for _, _, src in self._inputs())
 
     def step(self) -> int:
         """Enqueue train (both kinds, concurrently) + predict on the current
@@ -190,20 +229,31 @@ class DeviceWorkload:
             check(so.bbml_predict(ptr(self.pred_tab), len(self.pred_tab), ptr(self.Xq),
                                   self.wl.test.stride, ptr(self.weights), None, ptr(self.pred),
                                   main.cuda_stream), "bbml_predict")
-            launches += 1
+            check(so.bbml_metrics(ptr(self.met_tab), len(self.met_tab), ptr(self.pred),
+                                  ptr(self.yq), ptr(self.yq_raw), ptr(self.norms), ptr(self.metrics),
+                                  main.cuda_stream), "bbml_metrics")
+            launches += 2
         return launches
 
-    def fetch(self) -> dict:
+    def fetch(self, predictions: bool = True) -> dict:
+        """Weights, status and per-model metrics ((M, 4): mse, pearson,
+        spearman, done); with ``predictions`` also every test prediction."""
         out = {
             "weights": self.weights.cpu().numpy(),
             "status": self.status.cpu().numpy().view(STATUS)[: self.wl.n_models].copy(),
-            "pred": self.pred.cpu().numpy(),
+            "metrics": self.metrics.cpu().numpy()[: 4 * self.wl.n_models].reshape(-1, 4),
         }
+        if predictions:
+            out["pred"] = self.pred.cpu().numpy()
         return out
+
+    def d2h_bytes_for(self, predictions: bool = True) -> int:
+        return (self.weights.numel() * 8 + self.status.numel() + self.metrics.numel() * 8 +
+                (self.pred.numel() * 8 if predictions else 0))
 
     @property
     def d2h_bytes(self) -> int:
-        return (self.weights.numel() * 8 + self.status.numel() + self.pred.numel() * 8)
+        return self.d2h_bytes_for(True)
 
 
 def _launches_pnn(tab) -> int:
@@ -230,11 +280,18 @@ class HostBuffers:
         self.X = torch.from_numpy(np.ascontiguousarray(wl.train.X)).pin_memory()
         self.y = torch.from_numpy(np.ascontiguousarray(wl.train.y)).pin_memory()
         self.Xq = torch.from_numpy(np.ascontiguousarray(wl.test.X)).pin_memory()
+        # test targets (normalised + raw) and normaliser rows for the device metrics
+        self.yq = torch.from_numpy(np.ascontiguousarray(wl.test.y, dtype=np.float64)).pin_memory()
+        raw = wl.test_raw_y if wl.test_raw_y is not None else np.zeros(0)
+        self.yq_raw = torch.from_numpy(np.ascontiguousarray(raw, dtype=np.float64)).pin_memory()
+        self.norms = torch.from_numpy(np.ascontiguousarray(wl.norm_rows()).ravel()).pin_memory()
 
 
-def fit_predict(wl: Workload, dev: Optional[DeviceWorkload] = None) -> dict:
-    """End-to-end: H2D of the inputs, train every model, predict, D2H results."""
+def fit_predict(wl: Workload, dev: Optional[DeviceWorkload] = None,
+                predictions: bool = True) -> dict:
+    """End-to-end: H2D of the inputs, train every model, predict, per-model
+    metrics, D2H of weights / status / metrics (+ predictions)."""
     dev = DeviceWorkload(wl) if dev is None else dev
     dev.upload()
     dev.step()
-    return dev.fetch()
+    return dev.fetch(predictions)

@@ -18,7 +18,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libbbml.so"
-SOURCES = ["capi.cu", "pnn_train.cu", "lm_train.cu", "lm_wide.cu", "predict.cu", "units.cu"]
+SOURCES = ["capi.cu", "pnn_train.cu", "lm_train.cu", "lm_wide.cu", "predict.cu", "units.cu",
+           "metrics.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -258,3 +258,35 @@ def predict(weights_dev, w_offset, d, h, kind, Xq: Packed, norms: Optional[np.nd
     check(lib().bbml_predict(ptr(t), M, ptr(Xd), Xq.stride, ptr(weights_dev), ptr(nd), ptr(out),
                              _stream(torch)), "bbml_predict")
     return out.cpu().numpy()[:int(Xq.n.sum())]
+
+
+def metrics(pred, actual_norm, actual_raw, pred_offset, row_begin, n, d, norms, device=None):
+    """Per-model test metrics on the device (``bbml_metrics``):
+    for model i, predictions pred[pred_offset[i] : +n[i]] (normalised) against
+    actual_norm / actual_raw[row_begin[i] : +n[i]]; ``norms`` is (M, 2*d_max+2)
+    rows of [x_min(d), x_max(d), y_min, y_max].  Arrays may be host arrays or
+    device tensors.  Returns (M, 4) host float64: mse, pearson, spearman (NaN =
+    undefined) and a done flag (0: Pearson / Spearman left to the host, n > 4096)."""
+    torch = torch_cuda()
+    dev = torch.device("cuda" if device is None else device)
+
+    def on_dev(a):
+        if torch.is_tensor(a):
+            return a
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+
+    M = len(n)
+    norms = np.ascontiguousarray(norms, dtype=np.float64)
+    t = np.zeros(M, dtype=PRED_TASK)
+    t["row_begin"] = row_begin
+    t["n"] = n
+    t["w_offset"] = pred_offset
+    t["d"] = d
+    t["h"] = 1
+    t["norm_offset"] = np.arange(M, dtype=np.int64) * norms.shape[1]
+    t["out_offset"] = np.arange(M, dtype=np.int64) * 4
+    pd, an, ar, nd = on_dev(pred), on_dev(actual_norm), on_dev(actual_raw), on_dev(norms.ravel())
+    out = torch.empty(max(4 * M, 1), dtype=torch.float64, device=dev)
+    check(lib().bbml_metrics(ptr(t), M, ptr(pd), ptr(an), ptr(ar), ptr(nd), ptr(out),
+                             _stream(torch)), "bbml_metrics")
+    return out.cpu().numpy()[:4 * M].reshape(M, 4)

@@ -356,3 +356,48 @@ def test_br_hidden1_long_series_multiwarp():
         if abs(r.mse - o.mse) <= 1e-12 or _rel(r.pred_raw, o.pred_raw, floor) <= 1e-6:
             continue
         assert abs(r.mse - o.mse) <= 0.005, (k, r.mse, o.mse)
+
+
+def test_device_metrics_match_metrics_py():
+    """bbml_metrics against metrics.py: MSE in the normalised
+    space, Pearson / Spearman (average-rank ties) of de-normalised predictions
+    vs raw counts, undefined -> NaN / None; random and tie-heavy vectors,
+    constant vectors, n = 1, and a > 4096-row set left to the host."""
+    from paper_2202_07798_b200 import engine, metrics
+
+    rng = np.random.default_rng(4)
+    sizes = [1, 2, 3, 7, 50, 333, 1000, 4096, 5000]
+    preds, an, ar, norms, ds = [], [], [], [], []
+    for k, n in enumerate(sizes):
+        p = rng.normal(size=n)
+        a = rng.normal(size=n)
+        if k % 3 == 1:
+            p = np.round(p, 1)  # ties
+            a = np.round(a * 2) / 2
+        if k == 2:
+            a = np.full(n, 0.25)  # constant actual -> undefined correlations
+        lo, hi = rng.uniform(-5, 5), rng.uniform(6, 50)
+        preds.append(p)
+        an.append(a)
+        ar.append(np.round(a * (hi - lo) + lo, 3))
+        norms.append([0.0, 1.0, lo, hi])
+        ds.append(1)
+    off = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    out = engine.metrics(np.concatenate(preds), np.concatenate(an), np.concatenate(ar), off, off,
+                         np.array(sizes, np.int32), np.array(ds, np.int32), np.array(norms))
+    for k, n in enumerate(sizes):
+        p, a, raw = preds[k], an[k], ar[k]
+        lo, hi = norms[k][2], norms[k][3]
+        assert abs(out[k, 0] - metrics.mse(p, a)) <= 1e-12 * max(1.0, metrics.mse(p, a))
+        if n < 2:
+            assert np.isnan(out[k, 1]) and np.isnan(out[k, 2]) and out[k, 3] == 1.0
+            continue
+        if n > 4096:
+            assert out[k, 3] == 0.0
+            continue
+        pr = p * (hi - lo) + lo
+        for col, ref in ((1, metrics.pearson(pr, raw)), (2, metrics.spearman(pr, raw))):
+            if ref is None:
+                assert np.isnan(out[k, col]), (n, col)
+            else:
+                assert abs(out[k, col] - ref) <= 1e-12, (n, col, out[k, col], ref)
