@@ -272,7 +272,8 @@ struct alignas(16) WarpLm {
   // the tridiagonal (dd, e2, ee) here; the per-entry statistics tables and the
   // Jacobi schedule exist for PM = 8 only (smaller footprint -> more warps/SM)
   static constexpr bool kWide = PM > 8;
-  static constexpr int JCH = kWide ? 3 : 32;  // staged Jacobian rows per chunk (PM = 8)
+  static constexpr int JCH = kWide ? 5 : 32;  // staged Jacobian rows per chunk (PM = 8);
+                                              // PM = 32: dd, e2, ee, {d, e^2} rows
   double Jc[JCH * PM];
   double rc[kWide ? 2 : JCH];
   double cs[kWide ? 2 : 2 * 16];
@@ -875,12 +876,13 @@ __device__ double w_gamma_tri(WarpLm<PM>& S, int P, double alpha, double beta, i
   }
   __syncwarp();
   const double hi0 = (ghi + 2.220446049250313e-16 * tnorm) * scale;
-  // pad T to PM rows (d = 2 > ||T||, e = 0) for the fixed-length Sturm loop
-  if (lane >= P && lane < PM) dd[lane] = 2.0;
-  if (lane + 1 >= P && lane < PM) e2[lane] = 0.0;
+  // T padded to PM rows (d = 2 > ||T||, e = 0), rows as {d_j, e_{j-1}^2}
+  double2* de = (double2*)(S.Jc + 3 * PM);
+  if (lane < PM) de[lane] = make_double2(lane < P ? dd[lane] : 2.0,
+                                         (lane >= 1 && lane < P) ? e2[lane - 1] : 0.0);
   __syncwarp();
-  const int n_tiny = sturm_count_fixed<PM>(dd, e2, kSturmTiny);
-  const double part = lane < P ? sturm_gamma_part_fixed<PM>(dd, e2, lane, n_tiny, hi0,
+  const int n_tiny = sturm_count_fixed<PM>(de, kFixTiny);
+  const double part = lane < P ? sturm_gamma_part_fixed<PM>(de, lane, n_tiny, hi0,
                                                             alpha / beta * scale, 1.0 / scale,
                                                             alpha, beta)
                                : 0.0;

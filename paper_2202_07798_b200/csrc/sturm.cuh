@@ -60,50 +60,55 @@ __device__ __forceinline__ int sturm_count(const double* __restrict__ dd,
 
 // Fixed-length variant for the warp path (P <= PM <= 32): T padded to PM
 // rows with d = 2 (> ||T||), e = 0, so the fully unrolled loop needs no
-// bounds and the padding never changes sign (dd/e2 in shared memory: the
-// broadcast loads are off the recurrence's dependency chain).  Pivot floor every row; the pair
-// is renormalised by its exponent every second row (the floor bounds the
-// per-row shrink by 2^-400, bisection points stay >= 2^-300, so two rows
-// cannot leave the normal range).
+// bounds and the padding never changes sign.  de[j] = {d_j, e_{j-1}^2} in
+// shared memory (one 16-byte broadcast load per row, off the dependency
+// chain).  Bisection points stay >= 2^-200 and the pivot floor is 2^-200, so
+// a row shrinks the pair by at most 2^-200 and grows it by at most 3: the pair
+// is renormalised by its exponent every fourth row.
+constexpr double kFixPiv = 0x1p-200;
+constexpr double kFixTiny = 0x1p-200;  // scaled eigenvalues below this contribute 0
+
 template <int PM>
-__device__ __forceinline__ int sturm_count_fixed(const double* __restrict__ dd,
-                                                 const double* __restrict__ e2, double x) {
-  double p0 = 1.0, p1 = dd[0] - x;
-  p1 = fabs(p1) < kSturmPiv ? -kSturmPiv : p1;
+__device__ __forceinline__ int sturm_count_fixed(const double2* __restrict__ de, double x) {
+  double p0 = 1.0, p1 = de[0].x - x;
+  p1 = fabs(p1) < kFixPiv ? -kFixPiv : p1;
   int cnt = (int)((unsigned)__double2hiint(p1) >> 31);
   auto row = [&](int j) {
-    const double fl = kSturmPiv * p1;
-    double p2 = fma(dd[j] - x, p1, -(e2[j - 1] * p0));
+    const double2 v = de[j];
+    const double fl = kFixPiv * p1;
+    double p2 = fma(v.x - x, p1, -(v.y * p0));
     p2 = fabs(p2) < fabs(fl) ? -fl : p2;
     cnt += (int)((unsigned)(__double2hiint(p2) ^ __double2hiint(p1)) >> 31);
     p0 = p1;
     p1 = p2;
   };
-#pragma unroll 2
-  for (int j = 1; j < PM; j += 2) {
+  int j = 1;
+#pragma unroll 1
+  for (; j + 3 < PM; j += 4) {
     row(j);
-    if (j + 1 < PM) row(j + 1);
+    row(j + 1);
+    row(j + 2);
+    row(j + 3);
     const int hm = max(__double2hiint(p0) & 0x7fffffff, __double2hiint(p1) & 0x7fffffff);
     const double sc = __hiloint2double((2046 - (hm >> 20)) << 20, 0);
     p0 *= sc;
     p1 *= sc;
   }
+#pragma unroll
+  for (; j < PM; ++j) row(j);
   return cnt;
 }
 
-constexpr double kSturmTiny = 0x1p-300;  // scaled eigenvalues below this contribute 0
-
 // warp path: gamma contribution of the k-th smallest eigenvalue; n_tiny =
-// sturm_count_fixed(kSturmTiny) (eigenvalues below it, negative ones included,
-// are clipped to 0 -- their contribution is < 2^-300 / r)
+// sturm_count_fixed(kFixTiny) (eigenvalues below it, negative ones included,
+// are clipped to 0 -- their contribution is < 2^-200 / r)
 template <int PM>
-__device__ __forceinline__ double sturm_gamma_part_fixed(const double* __restrict__ dd,
-                                                         const double* __restrict__ e2, int k,
-                                                         int n_tiny,
-                                                       double hi0, double r, double inv_scale,
-                                                       double alpha, double beta) {
-  if (k < n_tiny || !(hi0 > kSturmTiny)) return 0.0;
-  double lo = kSturmTiny, hi = hi0;
+__device__ __forceinline__ double sturm_gamma_part_fixed(const double2* __restrict__ de, int k,
+                                                         int n_tiny, double hi0, double r,
+                                                         double inv_scale, double alpha,
+                                                         double beta) {
+  if (k < n_tiny || !(hi0 > kFixTiny)) return 0.0;
+  double lo = kFixTiny, hi = hi0;
   long long lb = __double_as_longlong(lo), hb = __double_as_longlong(hi0);
   constexpr double eps = 2.220446049250313e-16;
   // gamma pin: 1e-13 per eigenvalue for P <= 8 (hidden-1 fits, gated at 1e-6
@@ -116,7 +121,7 @@ __device__ __forceinline__ double sturm_gamma_part_fixed(const double* __restric
     if (w * r <= pin * ((hi + r) * (lo + r))) break;
     const long long mb = (lb + hb) >> 1;
     const double mid = __longlong_as_double(mb);
-    if (sturm_count_fixed<PM>(dd, e2, mid) > k) {
+    if (sturm_count_fixed<PM>(de, mid) > k) {
       hi = mid;
       hb = mb;
     } else {
