@@ -29,7 +29,13 @@ struct ForkPool {
   std::vector<cudaStream_t> streams;
   std::vector<cudaEvent_t> events;
   cudaEvent_t fork = nullptr;
+  unsigned cursor = 0;
 };
+// Child streams are handed out round-robin from kForkStreams, so two calls in
+// flight at once (bbml_lm_train on one stream and bbml_pnn_train on another,
+// as batch.DeviceWorkload.step issues them) get disjoint children instead of
+// queueing a PNN bucket behind an LM bucket on a shared child stream.
+constexpr int kForkStreams = 16;
 thread_local std::vector<ForkPool> g_pools;  // per device, per host thread
 }  // namespace
 
@@ -40,18 +46,21 @@ StreamFork::StreamFork(cudaStream_t parent, int n) : parent_(parent), n_(n) {
   if ((int)g_pools.size() <= dev) g_pools.resize(dev + 1);
   ForkPool& p = g_pools[dev];
   if (!p.fork) cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming);
-  while ((int)p.streams.size() < n_) {
-    cudaStream_t s;
+  while ((int)p.events.size() < n_) {
     cudaEvent_t e;
-    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    p.streams.push_back(s);
     p.events.push_back(e);
   }
   cudaEventRecord(p.fork, parent_);
   for (int i = 0; i < n_; ++i) {
-    cudaStreamWaitEvent(p.streams[i], p.fork, 0);
-    kids_.push_back(p.streams[i]);
+    const int k = (int)(p.cursor++ % kForkStreams);
+    if ((int)p.streams.size() <= k) {
+      cudaStream_t s;
+      cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+      p.streams.push_back(s);
+    }
+    cudaStreamWaitEvent(p.streams[k], p.fork, 0);
+    kids_.push_back(p.streams[k]);
     done_.push_back(p.events[i]);
   }
 }
