@@ -192,6 +192,7 @@ class DeviceWorkload:
         mt["out_offset"] = np.arange(wl.n_models, dtype=np.int64) * 4
         self.met_tab = mt
         self.metrics = torch.empty(max(4 * wl.n_models, 1), dtype=torch.float64, device=dev)
+        self._pinned_out = None
 
     def _inputs(self):
         return (("X", self.X, self.host.X), ("y", self.y, self.host.y), ("Xq", self.Xq, self.host.Xq),
@@ -249,13 +250,23 @@ class DeviceWorkload:
     def fetch(self, predictions: bool = True) -> dict:
         """Weights, status and per-model metrics ((M, 4): mse, pearson,
         spearman, done); with ``predictions`` also every test prediction."""
+        torch = self.torch
+        names = ("weights", "status", "metrics") + (("pred",) if predictions else ())
+        if self._pinned_out is None:
+            self._pinned_out = {}
+        for k in names:  # pinned staging buffers, allocated once per workload
+            if k not in self._pinned_out:
+                self._pinned_out[k] = torch.empty_like(getattr(self, k), device="cpu", pin_memory=True)
+            self._pinned_out[k].copy_(getattr(self, k), non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        h = {k: self._pinned_out[k].numpy().copy() for k in names}
         out = {
-            "weights": self.weights.cpu().numpy(),
-            "status": self.status.cpu().numpy().view(STATUS)[: self.wl.n_models].copy(),
-            "metrics": self.metrics.cpu().numpy()[: 4 * self.wl.n_models].reshape(-1, 4),
+            "weights": h["weights"],
+            "status": h["status"].view(STATUS)[: self.wl.n_models].copy(),
+            "metrics": h["metrics"][: 4 * self.wl.n_models].reshape(-1, 4),
         }
         if predictions:
-            out["pred"] = self.pred.cpu().numpy()
+            out["pred"] = h["pred"]
         return out
 
     def d2h_bytes_for(self, predictions: bool = True) -> int:
