@@ -709,6 +709,72 @@ __device__ bool w_solve_cols(WarpLm<PM>& S, int P, double alpha, double beta, do
   return true;
 }
 
+// Damped solve on the tridiagonal form w_gamma_tri leaves behind (P <= 32
+// path, hidden >= 2).  The LM trials of epoch e use the J'J that epoch e-1's
+// evidence update tridiagonalised: J'J = Q T Q', Q = H_0 ... H_{P-3},
+// H_k = I - bh_k v_k v_k' (v_k in column k below the diagonal of S.A, bh_k at
+// S.A[k][k+1], T = diag(S.A) + off-diagonal ee), so
+//   (beta J'J + (mu + alpha) I) delta = -g   <=>   delta = Q M^-1 Q' (-g),
+//   M = beta T + (mu + alpha) I  (SPD tridiagonal),
+// with g = beta J'r + alpha w (brbpnn.py:153-171).  Q'(-g) is formed once per
+// epoch (first trial); each trial is an LDL' of M (2P sequential steps) and
+// the back-transform -- O(P^2) instead of the LU's O(P^3) with a pivot
+// search per column.  Backward stable (orthogonal Q, SPD M); returns false
+// if a pivot of M is not positive (J'J numerically indefinite against a tiny
+// damping), and the caller falls back to the LU (w_solve_cols).
+template <int PM>
+__device__ bool w_solve_tri(WarpLm<PM>& S, int P, double alpha, double beta, double mu, int lane,
+                            bool first) {
+  constexpr int LD = WarpLm<PM>::LD;
+  const unsigned FULL = 0xffffffffu;
+  const double* __restrict__ ee = S.Jc + 2 * PM;
+  if (first) {
+    double x = lane < P ? -__dadd_rn(__dmul_rn(beta, S.jtr[lane]), __dmul_rn(alpha, S.w[lane])) : 0.0;
+    for (int k = 0; k + 2 < P; ++k) {  // Q' = H_{P-3} ... H_0
+      const double vi = (lane > k && lane < P) ? S.A[lane * LD + k] : 0.0;
+      const double bh = S.A[k * LD + k + 1];
+      x = fma(-bh * warp_sum(vi * x), vi, x);
+    }
+    if (lane < P) S.rhs[lane] = x;
+    __syncwarp();
+  }
+  const double damp = __dadd_rn(mu, alpha);
+  double dp = 0.0, yp = 0.0, md = 1.0, my = 0.0;
+  bool ok = true;
+  for (int i = 0; i < P; ++i) {  // M = L D L', L y = z (every lane, lane i keeps d_i, y_i)
+    const double mii = fma(beta, S.A[i * LD + i], damp);
+    double di = mii, yi = S.rhs[i];
+    if (i > 0) {
+      const double off = beta * ee[i - 1];
+      const double l = off / dp;
+      di = fma(-l, off, mii);
+      yi = fma(-l, yp, yi);
+    }
+    ok = ok && di > 0.0;
+    if (lane == i) {
+      md = di;
+      my = yi;
+    }
+    dp = di;
+    yp = yi;
+  }
+  if (!ok) return false;
+  double x = 0.0, xn = 0.0;
+  for (int i = P - 1; i >= 0; --i) {  // D L' x = y
+    const double off = i + 1 < P ? beta * ee[i] : 0.0;
+    xn = __shfl_sync(FULL, (my - off * xn) / md, i);
+    if (lane == i) x = xn;
+  }
+  for (int k = P - 3; k >= 0; --k) {  // Q = H_0 ... H_{P-3}
+    const double vi = (lane > k && lane < P) ? S.A[lane * LD + k] : 0.0;
+    const double bh = S.A[k * LD + k + 1];
+    x = fma(-bh * warp_sum(vi * x), vi, x);
+  }
+  if (lane < P) S.delta[lane] = x;
+  __syncwarp();
+  return true;
+}
+
 // gamma from the eigenvalues of J'J: cyclic Jacobi, round-robin disjoint
 // pairs, rotations skipped below max(eps * max|diag|, 1e-15 sqrt|a_pp a_qq|)
 // (LAPACK dsyevd's eigenvalues carry the same eps * ||A|| absolute accuracy)
@@ -807,7 +873,10 @@ __device__ double w_gamma_tri(WarpLm<PM>& S, int P, double alpha, double beta, i
     const double x0 = S.A[(k + 1) * LD + k];
     const double tail = sig - x0 * x0;
     if (!(tail > 0.0)) {  // column already tridiagonal
-      if (lane == 0) ee[k] = x0;
+      if (lane == 0) {
+        ee[k] = x0;
+        if constexpr (WarpLm<PM>::kWide) S.A[k * LD + k + 1] = 0.0;  // H_k = I
+      }
       __syncwarp();
       continue;
     }
@@ -844,8 +913,12 @@ __device__ double w_gamma_tri(WarpLm<PM>& S, int P, double alpha, double beta, i
         ai[j + 3] = a3 - fma(vi, wv[j + 3], wi * v[j + 3]);
       }
       for (; j < P; ++j) ai[j] -= fma(vi, wv[j], wi * v[j]);
+      if constexpr (WarpLm<PM>::kWide) ai[k] = vi;  // reflector kept for w_solve_tri
     }
-    if (lane == 0) ee[k] = al;
+    if (lane == 0) {
+      ee[k] = al;
+      if constexpr (WarpLm<PM>::kWide) S.A[k * LD + k + 1] = bh;  // row k is final
+    }
     __syncwarp();
   }
   if (lane < P) dd[lane] = S.A[lane * LD + lane];
@@ -1023,6 +1096,7 @@ __global__ void __launch_bounds__(NW > 1 ? 32 * NW : (PM > 8 ? 96 : 128),
   double e_w = 0.0;
   for (int i = 0; i < P; ++i) e_w = fma(S.w[i], S.w[i], e_w);
   bool have_stats = false;
+  bool tri = false;  // P <= 32 path: S.A holds J'J's tridiagonal form + reflectors
   int code = BBML_MODEL_OK, trials = 0, epochs = 0, any_pinned = 0, stable = 0;
   double fail_mu = 0.0, last_mu = NAN, last_gamma = NAN;
   double prev_g = 0.0, prev_d = 0.0, prev_w = 0.0;
@@ -1033,17 +1107,30 @@ __global__ void __launch_bounds__(NW > 1 ? 32 * NW : (PM > 8 ? 96 : 128),
       LM_PROF_T(t0);
       stats();
       LM_PROF_ADD(0, t0);
+      tri = false;
     }
     const double f0 = __dadd_rn(__dmul_rn(beta, e_d), __dmul_rn(alpha, e_w));
     bool accepted = false;
+    bool tri_first = true;
     double td = 0.0, tw = 0.0;
     while (true) {
       ++trials;
       LM_PROF_T(t2);
       bool solved = true;
       if (lead) {
-        solved = PM > 8 ? w_solve_cols<PM>(S, P, alpha, beta, mu, lane)
-                        : w_solve<PM>(S, P, alpha, beta, mu, lane);
+        if constexpr (WarpLm<PM>::kWide) {
+          bool done = false;
+          if (tri) {
+            done = w_solve_tri<PM>(S, P, alpha, beta, mu, lane, tri_first);
+            tri_first = false;
+          }
+          if (!done) {
+            tri = false;  // the LU overwrites the reflectors
+            solved = w_solve_cols<PM>(S, P, alpha, beta, mu, lane);
+          }
+        } else {
+          solved = w_solve<PM>(S, P, alpha, beta, mu, lane);
+        }
         if (lane < P) S.wt[lane] = __dadd_rn(S.w[lane], S.delta[lane]);
       }
       if constexpr (NW > 1) {
@@ -1089,8 +1176,10 @@ __global__ void __launch_bounds__(NW > 1 ? 32 * NW : (PM > 8 ? 96 : 128),
       // P <= 5: cyclic Jacobi (converges in a few sweeps at this size);
       // P >= 6: Householder + bisection
       if (lead) {
-        if constexpr (WarpLm<PM>::kWide) gamma = w_gamma_tri<PM>(S, P, alpha, beta, lane);
-        else if (P >= 6) gamma = w_gamma_tri<PM>(S, P, alpha, beta, lane);
+        if constexpr (WarpLm<PM>::kWide) {
+          gamma = w_gamma_tri<PM>(S, P, alpha, beta, lane);
+          tri = true;
+        } else if (P >= 6) gamma = w_gamma_tri<PM>(S, P, alpha, beta, lane);
         else gamma = w_gamma<PM>(S, P, alpha, beta, lane);
       }
       if constexpr (NW > 1) {

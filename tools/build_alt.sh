@@ -8,7 +8,7 @@ git archive "$rev" paper_2202_07798_b200/csrc include | tar -x -C "$tmp"
 objs=()
 for s in capi pnn_train lm_train lm_wide predict units metrics; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 \
-    -I "$tmp/include" --expt-relaxed-constexpr -c "$tmp/paper_2202_07798_b200/csrc/$s.cu" -o "$tmp/$s.o" &
+    ${DEFS} -I "$tmp/include" --expt-relaxed-constexpr -c "$tmp/paper_2202_07798_b200/csrc/$s.cu" -o "$tmp/$s.o" &
   objs+=("$tmp/$s.o")
 done
 wait
