@@ -709,8 +709,8 @@ __device__ bool w_solve_cols(WarpLm<PM>& S, int P, double alpha, double beta, do
   return true;
 }
 
-// Damped solve on the tridiagonal form w_gamma_tri leaves behind (P <= 32
-// path, hidden >= 2).  The LM trials of epoch e use the J'J that epoch e-1's
+// Damped solve on the tridiagonal form w_gamma_tri leaves behind (warp
+// kernels, P >= 6: hidden-1 fits with d >= 3 and the P <= 32 path).  The LM trials of epoch e use the J'J that epoch e-1's
 // evidence update tridiagonalised: J'J = Q T Q', Q = H_0 ... H_{P-3},
 // H_k = I - bh_k v_k v_k' (v_k in column k below the diagonal of S.A, bh_k at
 // S.A[k][k+1], T = diag(S.A) + off-diagonal ee), so
@@ -875,7 +875,7 @@ __device__ double w_gamma_tri(WarpLm<PM>& S, int P, double alpha, double beta, i
     if (!(tail > 0.0)) {  // column already tridiagonal
       if (lane == 0) {
         ee[k] = x0;
-        if constexpr (WarpLm<PM>::kWide) S.A[k * LD + k + 1] = 0.0;  // H_k = I
+        S.A[k * LD + k + 1] = 0.0;  // H_k = I
       }
       __syncwarp();
       continue;
@@ -913,11 +913,11 @@ __device__ double w_gamma_tri(WarpLm<PM>& S, int P, double alpha, double beta, i
         ai[j + 3] = a3 - fma(vi, wv[j + 3], wi * v[j + 3]);
       }
       for (; j < P; ++j) ai[j] -= fma(vi, wv[j], wi * v[j]);
-      if constexpr (WarpLm<PM>::kWide) ai[k] = vi;  // reflector kept for w_solve_tri
+      ai[k] = vi;  // reflector kept for w_solve_tri
     }
     if (lane == 0) {
       ee[k] = al;
-      if constexpr (WarpLm<PM>::kWide) S.A[k * LD + k + 1] = bh;  // row k is final
+      S.A[k * LD + k + 1] = bh;  // row k is final
     }
     __syncwarp();
   }
@@ -1096,7 +1096,7 @@ __global__ void __launch_bounds__(NW > 1 ? 32 * NW : (PM > 8 ? 96 : 128),
   double e_w = 0.0;
   for (int i = 0; i < P; ++i) e_w = fma(S.w[i], S.w[i], e_w);
   bool have_stats = false;
-  bool tri = false;  // P <= 32 path: S.A holds J'J's tridiagonal form + reflectors
+  bool tri = false;  // P >= 6: S.A holds the tridiagonal form + reflectors of J'J
   int code = BBML_MODEL_OK, trials = 0, epochs = 0, any_pinned = 0, stable = 0;
   double fail_mu = 0.0, last_mu = NAN, last_gamma = NAN;
   double prev_g = 0.0, prev_d = 0.0, prev_w = 0.0;
@@ -1118,18 +1118,15 @@ __global__ void __launch_bounds__(NW > 1 ? 32 * NW : (PM > 8 ? 96 : 128),
       LM_PROF_T(t2);
       bool solved = true;
       if (lead) {
-        if constexpr (WarpLm<PM>::kWide) {
-          bool done = false;
-          if (tri) {
-            done = w_solve_tri<PM>(S, P, alpha, beta, mu, lane, tri_first);
-            tri_first = false;
-          }
-          if (!done) {
-            tri = false;  // the LU overwrites the reflectors
-            solved = w_solve_cols<PM>(S, P, alpha, beta, mu, lane);
-          }
-        } else {
-          solved = w_solve<PM>(S, P, alpha, beta, mu, lane);
+        bool done = false;
+        if (tri) {
+          done = w_solve_tri<PM>(S, P, alpha, beta, mu, lane, tri_first);
+          tri_first = false;
+        }
+        if (!done) {
+          tri = false;  // the LU overwrites the reflectors
+          solved = PM > 8 ? w_solve_cols<PM>(S, P, alpha, beta, mu, lane)
+                          : w_solve<PM>(S, P, alpha, beta, mu, lane);
         }
         if (lane < P) S.wt[lane] = __dadd_rn(S.w[lane], S.delta[lane]);
       }
@@ -1179,7 +1176,10 @@ __global__ void __launch_bounds__(NW > 1 ? 32 * NW : (PM > 8 ? 96 : 128),
         if constexpr (WarpLm<PM>::kWide) {
           gamma = w_gamma_tri<PM>(S, P, alpha, beta, lane);
           tri = true;
-        } else if (P >= 6) gamma = w_gamma_tri<PM>(S, P, alpha, beta, lane);
+        } else if (P >= 6) {
+          gamma = w_gamma_tri<PM>(S, P, alpha, beta, lane);
+          tri = true;
+        }
         else gamma = w_gamma<PM>(S, P, alpha, beta, lane);
       }
       if constexpr (NW > 1) {
