@@ -983,9 +983,17 @@ __device__ unsigned long long g_lm_prof[8];
 // hidden-1 d <= 2 models are short and numerous -> 6 (80 registers, spills
 // cheaper than the latency they hide); d >= 3 includes the longest series
 // (pathfinder n = 7604), where spills would lengthen the critical chain -> 4
+// PM = 32: 19.5 KB of shared memory per warp.  1-warp CTAs (+1 KB reserved
+// each) pack 11 warps per SM; 3-warp CTAs (58.6 KB) only 9.
+#ifndef LM32_WARPS
+#define LM32_WARPS 1
+#endif
+#ifndef LM32_MINB
+#define LM32_MINB (LM32_WARPS == 1 ? 11 : 4)
+#endif
 template <int PM, int D>
 constexpr int lm_min_blocks() {
-  return PM > 8 ? 4 : (D == 1 || D == 2) ? 6 : 4;  // PM = 32: 3-warp CTAs, 4 per SM (shared memory)
+  return PM > 8 ? LM32_MINB : (D == 1 || D == 2) ? 6 : 4;
 }
 // NW = 1: one model per warp.  NW > 1 (hidden-1 long series): one model per
 // CTA of NW warps -- the per-sample passes (objective, J'J / J'r) are split
@@ -993,7 +1001,7 @@ constexpr int lm_min_blocks() {
 // damped solve and the eigen-solve run on warp 0; the scalar LM / evidence
 // bookkeeping is computed identically by every warp.
 template <int PM, int D, int NW = 1>
-__global__ void __launch_bounds__(NW > 1 ? 32 * NW : (PM > 8 ? 96 : 128),
+__global__ void __launch_bounds__(NW > 1 ? 32 * NW : (PM > 8 ? 32 * LM32_WARPS : 128),
                                   NW > 1 ? 1 : lm_min_blocks<PM, D>()) lm_warp_kernel(LmLaunch L) {
   extern __shared__ __align__(16) unsigned char lm_smem[];
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
@@ -1252,7 +1260,7 @@ __global__ void __launch_bounds__(NW > 1 ? 32 * NW : (PM > 8 ? 96 : 128),
 
 template <int PM, int D>
 static cudaError_t lm_launch_warp(const LmLaunch& L, cudaStream_t s) {
-  const int warps = PM > 8 ? 3 : 4;  // PM = 32: 19 KB smem per warp -> 3-warp CTAs pack 12 warps per SM
+  const int warps = PM > 8 ? LM32_WARPS : 4;
   const size_t smem = warps * sizeof(WarpLm<PM>);
   auto k = lm_warp_kernel<PM, D>;
   if (smem > 48 * 1024) {
