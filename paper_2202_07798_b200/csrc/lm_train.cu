@@ -983,13 +983,15 @@ __device__ unsigned long long g_lm_prof[8];
 // hidden-1 d <= 2 models are short and numerous -> 6 (80 registers, spills
 // cheaper than the latency they hide); d >= 3 includes the longest series
 // (pathfinder n = 7604), where spills would lengthen the critical chain -> 4
-// PM = 32: 19.5 KB of shared memory per warp.  1-warp CTAs (+1 KB reserved
-// each) pack 11 warps per SM; 3-warp CTAs (58.6 KB) only 9.
+// PM = 32: 19.5 KB of shared memory per warp (+2 KB static / reserved per
+// CTA).  2-warp CTAs pack 5 x 2 = 10 warps per SM, 3-warp CTAs only 3 x 3;
+// A/B on one box (tools/ab_step.sh): gramschmit BR 268 -> 258 ms, suite16
+// step 854 -> 825 ms; 1-warp CTAs (10 per SM) measured 274 / 843 ms.
 #ifndef LM32_WARPS
-#define LM32_WARPS 1
+#define LM32_WARPS 2
 #endif
 #ifndef LM32_MINB
-#define LM32_MINB (LM32_WARPS == 1 ? 11 : 4)
+#define LM32_MINB 5
 #endif
 template <int PM, int D>
 constexpr int lm_min_blocks() {
