@@ -1274,8 +1274,14 @@ static cudaError_t lm_launch_warp(const LmLaunch& L, cudaStream_t s) {
 }
 
 // hidden-1 long series: one model per CTA of LM_NW warps
-constexpr int LM_NW = 4;
-constexpr int kLongLm = 2048;  // samples from which a hidden-1 fit gets a CTA
+#ifndef BBML_LM_NW
+#define BBML_LM_NW 4
+#endif
+#ifndef BBML_LONG_LM
+#define BBML_LONG_LM 2048
+#endif
+constexpr int LM_NW = BBML_LM_NW;
+constexpr int kLongLm = BBML_LONG_LM;  // samples from which a hidden-1 fit gets a CTA
 template <int D>
 static cudaError_t lm_launch_multi(const LmLaunch& L, cudaStream_t s) {
   const size_t smem = sizeof(WarpLm<8>) + (size_t)(LM_NW * 64 + 8) * sizeof(double);
