@@ -93,6 +93,8 @@ def forward(model: BrbpnnModel, x: np.ndarray) -> Union[float, np.ndarray]:
     x = np.asarray(x, dtype=float)
     single = x.ndim == 1
     X = np.atleast_2d(x)
+    if X.shape[1] != model.n_inputs:  # the reference's X @ W1.T raises here
+        raise ValueError(f"forward: expected {model.n_inputs} input columns, got {X.shape[1]}")
     out = engine.predict(pack(model), np.array([0]), model.n_inputs, model.hidden, 1,
                          engine.pack([X]))
     return float(out[0]) if single else out

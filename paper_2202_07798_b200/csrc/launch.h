@@ -29,6 +29,10 @@ struct PnnLaunch {
   int32_t perm_in_smem;    // 1: permutation double buffers live in shared memory
   int32_t perm_cap;        // elements per smem permutation buffer (max n of the launch)
   int32_t groups_per_cta;  // models per CTA (consumer groups; producer lane i serves group i)
+  int32_t poll_cap_ns;     // producer poll back-off cap (ns)
+  int32_t stage_off;       // FP64 kernel: byte offset of the row staging area in shared memory
+  const double2* bc;       // FP64 kernel: Adam bias corrections {1 - 0.9^t, 1 - 0.999^t}, t = 1..bc_len
+  int32_t bc_len;          //   (host libm pow, as the reference's Python float pow); 1.0 beyond
 };
 
 struct LmLaunch {

@@ -26,9 +26,12 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
+#include "f64math.cuh"
 #include "launch.h"
 #include "pcg64.cuh"
 
@@ -169,6 +172,7 @@ __device__ void perm_producer_warp(const PnnLaunch& L, int groups, int pw, int n
     }
   }
   __syncwarp();
+  unsigned sleep_ns = 100;
   while (true) {
     bool alive = false, progress = false;
     for (int m = pw; m < groups; m += npw) {
@@ -254,9 +258,17 @@ __device__ void perm_producer_warp(const PnnLaunch& L, int groups, int pw, int n
       progress = true;
     }
     if (!alive) break;
-    // short poll: epochs of short series take ~10 us (a 2 us poll measured
-    // slower on app20 and no faster on the long series)
-    if (!progress) __nanosleep(100);
+    // FP32: short fixed poll (epochs of short series take ~10 us; a 2 us poll
+    // measured slower on app20).  FP64 epochs are several times longer and
+    // the spinning producer steals issue slots from the consumer warps of
+    // its SM sub-partition, so the poll backs off exponentially up to
+    // L.poll_cap_ns and resets whenever an epoch was produced.
+    if (!progress) {
+      __nanosleep(sleep_ns);
+      sleep_ns = min(2 * sleep_ns, (unsigned)L.poll_cap_ns);
+    } else {
+      sleep_ns = 100;
+    }
   }
 }
 
@@ -884,6 +896,402 @@ __device__ __forceinline__ void pnn_lat_body(const PnnLaunch& L) {
   }
 }
 
+// ------------------------------------------------------------------------
+// FP64 trainer for h <= 16 (the drop-in's default arithmetic and the bench
+// headline).  Same warp-per-model lane map as pnn_lat_body (lane = (sample
+// half sg, hidden unit j)) with numpy's elementwise rounding (no FMA
+// contraction in the elementwise chain), rebuilt around what an FP64 step
+// costs on sm_100a, where every FP64 instruction is issue-bound (64 FP64
+// lanes / SM) and the per-model chain is sequential:
+//   * Adam bias corrections 1 - beta^t come from a host table computed with
+//     libm pow (the value Python's float pow gives the reference,
+//     pnn.py:185-186) instead of two device pow() calls per step; beyond the
+//     table both are exactly 1.0 and the divisions by them are skipped
+//     (x / 1.0 == x exactly), which leaves one sqrt and one division per
+//     parameter for all but the first ~37k steps.
+//   * minibatch rows are staged into shared memory by cp.async (8-byte
+//     LDGSTS, one chunk ahead, per-warp double buffer) instead of being
+//     prefetched into registers: the row gather stays off the critical
+//     path without 2 x SP x (DM+1) doubles of live registers (the register
+//     prefetch spilled at DM = 4 in FP64).
+//   * each half-warp runs Adam for half of its unit's parameters; the
+//     gradient halves and the updated weights are exchanged with one
+//     xor-16 shuffle per parameter pair.
+// ------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// pnn.py:184-188 with numpy's rounding, branch-free (f64math.cuh).
+// BC = false: both bias corrections are exactly 1.0 (x / 1.0 == x), so the
+// two divisions by them are dropped.
+__device__ __forceinline__ double sqrt_any_bf(double x) {  // x >= 0, denormals included
+  const bool tiny = x < 0x1p-968;
+  const double s = sqrt_rn_bf(tiny ? x * 0x1p1000 : x);  // exact power-of-4 scaling
+  return tiny ? s * 0x1p-500 : s;
+}
+template <bool BC>
+__device__ __forceinline__ void adam_exact(double& p, double& m, double& v, double g, double bc1,
+                                           double bc2, double lr) {
+  m = __dadd_rn(__dmul_rn(0.9, m), __dmul_rn(1.0 - 0.9, g));
+  v = __dadd_rn(__dmul_rn(0.999, v), __dmul_rn(1.0 - 0.999, __dmul_rn(g, g)));
+  const double mh = BC ? div_rn_bf(m, bc1) : m;
+  const double vh = BC ? div_rn_bf(v, bc2) : v;
+  p = __dsub_rn(p, div_rn_bf(__dmul_rn(lr, mh), __dadd_rn(sqrt_any_bf(vh), 1e-8)));
+}
+
+// staging: per consumer warp, 2 buffers x 2 halves x SP rows x RW doubles
+template <int DM, int SP>
+__host__ __device__ constexpr int f64_stage_doubles() {
+  return 2 * 2 * SP * (DM + 1);
+}
+
+template <int DM, int SP, typename PermT>
+__device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
+  constexpr int RW = DM + 1;  // staged row: x[0..DM), y
+  constexpr int C = 2 * SP;   // samples per chunk (both halves)
+  constexpr int NP = DM + 2;  // per-unit parameters: w1[0..DM), b1, w2
+  const int groups = L.groups_per_cta;
+  const int cons_threads = groups * 32;
+  const int npw = ((int)blockDim.x - cons_threads) / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const PnnSmem SM = pnn_smem(smem_raw, groups, npw);
+  int* produced = SM.produced;
+  int* consumed = SM.consumed;
+  PermT* sperm = (PermT*)SM.perm;
+  double* stage_all = (double*)(smem_raw + L.stage_off);
+  for (int i = threadIdx.x; i < groups * f64_stage_doubles<DM, SP>(); i += blockDim.x) stage_all[i] = 0.0;
+  if (threadIdx.x < groups) {
+    produced[threadIdx.x] = 0;
+    consumed[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x >= cons_threads) {
+    const int pw = ((int)threadIdx.x - cons_threads) >> 5;
+    perm_producer_warp<PermT>(L, groups, pw, npw, produced, consumed, sperm, SM.pm, SM.ring + 64 * pw);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int gi = threadIdx.x >> 5;
+  const int64_t gid = (int64_t)blockIdx.x * groups + gi;
+  if (gid >= L.n_tasks) return;
+  const int sg = lane >> 4, j = lane & 15;
+  const unsigned FULL = 0xffffffffu;
+  double* stage = stage_all + gi * f64_stage_doubles<DM, SP>();
+
+  const bbml_pnn_task tk = L.tasks[gid];
+  const int orig = L.orig_index[gid];
+  const int n = tk.n, d = tk.d, h = tk.h, B = tk.batch;
+  const double* __restrict__ X = L.X + tk.row_begin * (int64_t)L.x_stride;
+  const double* __restrict__ Y = L.y + tk.row_begin;
+  const PermT* pbase = perm_smem<PermT>() ? sperm + (int64_t)gi * 2 * L.perm_cap
+                                      : (const PermT*)L.perm_global + 2 * L.perm_offset[gid];
+  const int64_t cap = perm_smem<PermT>() ? L.perm_cap : n;
+
+  // ---- init (pnn.py:97-104): unit j's parameters p[0..DM) = W1[j, :], p[DM] = b1[j], p[DM+1] = W2[j]
+  double p[NP], m1[NP], m2[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) p[q] = m1[q] = m2[q] = 0.0;
+  double b2, mb2 = 0.0, vb2 = 0.0;
+  {
+    Pcg64 rng;
+    rng.seed(tk.seed);
+    const double s1 = __ddiv_rn(1.0, __dsqrt_rn((double)d));
+    const double s2 = __ddiv_rn(1.0, __dsqrt_rn((double)h));
+    for (int jj = 0; jj < h; ++jj)
+      for (int k = 0; k < d; ++k) {
+        const double v = rng.uniform(-s1, s1);
+#pragma unroll
+        for (int kk = 0; kk < DM; ++kk)
+          if (jj == j && kk == k) p[kk] = v;
+      }
+    for (int jj = 0; jj < h; ++jj) {
+      const double v = rng.uniform(-s1, s1);
+      if (jj == j) p[DM] = v;
+    }
+    for (int jj = 0; jj < h; ++jj) {
+      const double v = rng.uniform(-s2, s2);
+      if (jj == j) p[DM + 1] = v;
+    }
+    b2 = rng.uniform(-s2, s2);
+  }
+  const double eps = tk.eps, lr = tk.lr;
+  int64_t t = 0;
+  int status = BBML_MODEL_OK, fail_epoch = 0, fail_block = 0;
+  double fail_value = 0.0;
+  const int nbatches = (n + B - 1) / B;
+
+  // lane's staging slots: element e = j and j + 16 of its half's SP x RW block
+  auto issue = [&](int buf, const PermT* perm, int off, int cnt) {
+    double* dst = stage + (buf * 2 + sg) * SP * RW;
+#pragma unroll
+    for (int rep = 0; rep < 2; ++rep) {
+      const int e = j + 16 * rep;
+      if (e < SP * RW) {
+        const int i = e / RW, k = e % RW;
+        const int c = sg * SP + i;
+        const int row = (int)perm[off + (c < cnt ? c : 0)];
+        if (k < d) cp_async8(dst + e, X + (int64_t)row * L.x_stride + k);
+        else if (k == DM) cp_async8(dst + e, Y + row);
+      }
+    }
+    cp_async_commit();
+  };
+
+  double g[NP], gb2, bloss;
+  auto zero_grads = [&]() {
+#pragma unroll
+    for (int q = 0; q < NP; ++q) g[q] = 0.0;
+    gb2 = bloss = 0.0;
+  };
+  for (int ep = 0; ep < tk.epochs; ++ep) {
+    while (ld_volatile(produced + gi) <= ep) {
+    }
+    __threadfence_block();
+    const PermT* perm = pbase + (ep & 1) * cap;
+    double eloss = 0.0;
+    zero_grads();
+    int bs = 0, s0 = 0, buf = 0;
+    issue(0, perm, 0, min(C, min(B, n)));
+    double2 bc = t < L.bc_len ? __ldg(L.bc + t) : make_double2(1.0, 1.0);
+    while (true) {
+      const int nb = min(B, n - bs);
+      const int cnt = min(C, nb - s0);
+      int nbs = bs, ns0 = s0 + C;
+      if (ns0 >= nb) {
+        nbs = bs + B;
+        ns0 = 0;
+      }
+      const bool more = nbs < n;
+      if (more) issue(buf ^ 1, perm, nbs + ns0, min(C, min(B, n - nbs) - ns0));
+      else cp_async_commit();  // empty group keeps wait_group 1 exact
+      cp_async_wait1();
+      __syncwarp();
+      const double* rows = stage + (buf * 2 + sg) * SP * RW;
+
+      // forward (own unit, own half's samples)
+      double a[SP], z[SP];
+#pragma unroll
+      for (int i = 0; i < SP; ++i) {
+        double pre = p[DM];
+#pragma unroll
+        for (int k = 0; k < DM; ++k) pre += p[k] * rows[i * RW + k];
+        a[i] = tanh_bf(pre);
+        z[i] = a[i] * p[DM + 1];
+      }
+#pragma unroll
+      for (int mm = 1; mm < 16; mm <<= 1)
+#pragma unroll
+        for (int i = 0; i < SP; ++i) z[i] += __shfl_xor_sync(FULL, z[i], mm);
+      // loss chain of sample (sg, j) on lane j < SP (pnn.py:131-138)
+      double zj = z[0];
+#pragma unroll
+      for (int i = 1; i < SP; ++i)
+        if (j == i) zj = z[i];
+      const double yj = j < SP ? rows[j * RW + DM] : 0.5;
+      const bool mine = j < SP && (sg * SP + j) < cnt;
+      const double nb_t = (double)nb;
+      const double zz = __dadd_rn(zj, b2);
+      const double sp = softplus(zz);
+      const double rate = __dadd_rn(sp, eps);
+      const double re = __dadd_rn(rate, eps);
+      // y == 0 (the series minimum after normalisation): 0 / re == 0 exactly,
+      // without the division's special-operand path
+      const double drate = div_rn_bf(__dsub_rn(1.0, div_rn_bf(yj, re)), nb_t);
+      const double dzj = mine ? __dmul_rn(drate, exp(__dsub_rn(zz, sp))) : 0.0;
+      if (mine) bloss += __dsub_rn(rate, __dmul_rn(yj, log(re)));
+      // backward (pnn.py:139-146)
+#pragma unroll
+      for (int i = 0; i < SP; ++i) {
+        const double dz = __shfl_sync(FULL, dzj, (lane & 16) | i);
+        gb2 += dz;
+        g[DM + 1] += a[i] * dz;
+        const double dp = __dmul_rn(__dmul_rn(dz, p[DM + 1]), __dsub_rn(1.0, __dmul_rn(a[i], a[i])));
+        g[DM] += dp;
+#pragma unroll
+        for (int k = 0; k < DM; ++k) g[k] += dp * rows[i * RW + k];
+      }
+      __syncwarp();  // every lane has read this staging buffer
+      buf ^= 1;
+      if (ns0 == 0) {  // end of minibatch: checks + Adam (pnn.py:243-247, 174-189)
+        // gradient halves: lane sg owns parameters q with q % 2 == sg; one
+        // xor-16 shuffle per pair sends the partner's partial sum and
+        // receives the partner's partial of an own parameter
+#pragma unroll
+        for (int q = 0; q < NP; q += 2) {
+          if (q + 1 < NP) {
+            const double send = sg ? g[q] : g[q + 1];
+            const double recv = __shfl_xor_sync(FULL, send, 16);
+            if (sg) g[q + 1] += recv;
+            else g[q] += recv;
+          } else {
+            g[q] += __shfl_xor_sync(FULL, g[q], 16);
+          }
+        }
+        gb2 += __shfl_xor_sync(FULL, gb2, 16);
+        bool bw1 = false, bb1 = false, bw2 = false;
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          const bool own = (q % 2 == sg) || (q + 1 == NP && NP % 2 == 1);
+          const bool bad = own && !isfinite(g[q]) && (q >= DM || q < d) && j < h;
+          if (q < DM) bw1 |= bad;
+          else if (q == DM) bb1 |= bad;
+          else bw2 |= bad;
+        }
+        const unsigned bits = (!isfinite(bloss) ? 1u : 0u) | (bw1 ? 2u : 0u) | (bb1 ? 4u : 0u) |
+                              (bw2 ? 8u : 0u) | (!isfinite(gb2) ? 16u : 0u);
+        const unsigned any = __reduce_or_sync(FULL, bits);
+        if (any) {
+          double lsum = bloss;
+#pragma unroll
+          for (int mm = 1; mm < 32; mm <<= 1) lsum += __shfl_xor_sync(FULL, lsum, mm);
+          const double loss = __ddiv_rn(lsum, nb_t);
+          if ((any & 1u) || !isfinite(loss)) {
+            status = BBML_MODEL_DIVERGED;
+            fail_epoch = ep;
+            fail_value = loss;
+            break;
+          }
+          status = BBML_MODEL_NONFINITE_GRAD;
+          fail_epoch = ep;
+          fail_block = (any & 2u) ? 0 : (any & 4u) ? 1 : (any & 8u) ? 2 : 3;
+          break;
+        }
+        ++t;
+        const double bc1 = bc.x, bc2 = bc.y;
+        bc = t < L.bc_len ? __ldg(L.bc + t) : make_double2(1.0, 1.0);  // next step's, early
+        // slot i of lane (sg, j) is parameter q = 2i + sg of unit j, so every
+        // lane runs the same NP/2 (branch-free, overlapping) updates; lanes
+        // of padded units / inputs compute on zeros and keep their values.
+        // b2 rides in slot 0 of the first padded unit's lane (h < 16) and is
+        // broadcast, else it takes one more slot on every lane.
+        const bool b2_slot = h < 16;
+        const bool b2_lane = b2_slot && sg == 0 && j == h;
+        auto adam_all = [&](auto bc_tag) {
+          constexpr bool BC = decltype(bc_tag)::value;
+#pragma unroll
+          for (int i = 0; i < NP / 2; ++i) {
+            const int q = 2 * i + sg;
+            const bool real = j < h && (q >= DM || q < d);
+            double pv = sg ? p[2 * i + 1] : p[2 * i];
+            double mv = sg ? m1[2 * i + 1] : m1[2 * i];
+            double vv = sg ? m2[2 * i + 1] : m2[2 * i];
+            double gv = sg ? g[2 * i + 1] : g[2 * i];
+            if (i == 0 && b2_lane) {
+              pv = b2;
+              mv = mb2;
+              vv = vb2;
+              gv = gb2;
+            }
+            adam_exact<BC>(pv, mv, vv, gv, bc1, bc2, lr);
+            if (i == 0 && b2_lane) {
+              b2 = pv;
+              mb2 = mv;
+              vb2 = vv;
+            } else if (real) {
+              if (sg) {
+                p[2 * i + 1] = pv;
+                m1[2 * i + 1] = mv;
+                m2[2 * i + 1] = vv;
+              } else {
+                p[2 * i] = pv;
+                m1[2 * i] = mv;
+                m2[2 * i] = vv;
+              }
+            }
+          }
+          if (b2_slot) b2 = __shfl_sync(FULL, b2, h);
+          else adam_exact<BC>(b2, mb2, vb2, gb2, bc1, bc2, lr);
+        };
+        if (bc1 != 1.0 || bc2 != 1.0) adam_all(std::true_type{});  // warp-uniform (t is per model)
+        else adam_all(std::false_type{});
+        // updated weights back to the partner half
+#pragma unroll
+        for (int q = 0; q + 1 < NP; q += 2) {
+          const double send = sg ? p[q + 1] : p[q];
+          const double recv = __shfl_xor_sync(FULL, send, 16);
+          if (sg) p[q] = recv;
+          else p[q + 1] = recv;
+        }
+        eloss += div_rn_bf(bloss, nb_t);  // this lane's share of the batch mean
+        zero_grads();
+      }
+      if (!more) break;
+      bs = nbs;
+      s0 = ns0;
+    }
+    __syncwarp();
+    if (status != BBML_MODEL_OK) break;
+    if (tk.hist_offset >= 0) {
+      double el = eloss;
+#pragma unroll
+      for (int mm = 1; mm < 32; mm <<= 1) el += __shfl_xor_sync(FULL, el, mm);
+      if (lane == 0) L.history[tk.hist_offset + ep] = el / nbatches;
+    }
+    if (lane == 0) {
+      __threadfence_block();
+      st_volatile(consumed + gi, ep + 1);
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (lane == 0) st_volatile(consumed + gi, kConsumedDone);
+
+  double* W = L.weights + tk.w_offset;
+  if (sg == 0 && j < h) {
+#pragma unroll
+    for (int kk = 0; kk < DM; ++kk)
+      if (kk < d) W[j * d + kk] = p[kk];
+    W[h * d + j] = p[DM];
+    W[h * d + h + j] = p[DM + 1];
+  }
+  if (lane == 0) {
+    W[h * d + 2 * h] = b2;
+    bbml_model_status st{};
+    st.code = status;
+    st.epochs = status == BBML_MODEL_OK ? tk.epochs : fail_epoch;
+    st.detail = fail_block;
+    st.value = fail_value;
+    L.status[orig] = st;
+  }
+}
+
+template <int DM, int SP, typename PermT>
+__global__ void __launch_bounds__(256, 1) pnn_f64_kernel(PnnLaunch L) {
+  pnn_f64_body<DM, SP, PermT>(L);
+}
+// short series: 4 consumer + 1 shared producer warp
+template <int DM, int SP, typename PermT>
+__global__ void __launch_bounds__(160, 3) pnn_f64_kernel_shared(PnnLaunch L) {
+  pnn_f64_body<DM, SP, PermT>(L);
+}
+template <int DM, int SP, typename PermT>
+__global__ void __launch_bounds__(160, 4) pnn_f64_kernel_shared4(PnnLaunch L) {
+  pnn_f64_body<DM, SP, PermT>(L);
+}
+// 4 consumer + 2 producer warps, 3 CTAs per SM
+template <int DM, int SP, typename PermT>
+__global__ void __launch_bounds__(192, 3) pnn_f64_kernel_np2(PnnLaunch L) {
+  pnn_f64_body<DM, SP, PermT>(L);
+}
+// FP64 CTA shapes (development knobs, defaults from one-box A/B):
+//   BBML_F64_LONG_NPW  = 1 | 2 | 4   producer warps per CTA for n >= kLongSeries
+//   BBML_F64_SHORT_MINB = 3 | 4      CTAs per SM for the shared-producer kernel
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+static int f64_long_npw() {
+  static const int v = env_int("BBML_F64_LONG_NPW", 4);
+  return v;
+}
+static int f64_short_minb() {
+  static const int v = env_int("BBML_F64_SHORT_MINB", 4);
+  return v;
+}
+
 // long series: 4 consumer + 4 producer warps, register allocation unconstrained
 template <typename T, int DM, int SP, typename PermT>
 __global__ void pnn_lat_kernel(PnnLaunch L) {
@@ -957,7 +1365,7 @@ static cudaError_t launch_variant(PnnLaunch L, int64_t nmax, size_t smem_limit, 
   // CTA is 5 warps and eight CTAs fit per SM.
   const bool shared_prod = LAT && nmax < kLongSeries;
   const int groups_max = 4;
-  const int npw_long = LAT ? long_npw() : groups_max;
+  const int npw_long = !LAT ? groups_max : sizeof(T) == 8 ? f64_long_npw() : long_npw();
   const int npw_max = shared_prod ? 1 : npw_long;
   const size_t flags = pnn_smem_header(groups_max, groups_max);
   const size_t per_group = 2 * (size_t)nmax * sizeof(PermT);
@@ -980,10 +1388,19 @@ static cudaError_t launch_variant(PnnLaunch L, int64_t nmax, size_t smem_limit, 
   const int cons = ((groups * G + 31) / 32) * 32;
   const int prod = 32 * npw;
   const int blocks = (int)ceil_div(L.n_tasks, groups);
+  constexpr bool F64 = LAT && sizeof(T) == 8;
+  if (F64) {  // per-warp row staging after the permutation buffers
+    L.stage_off = (int32_t)(16 * ((smem + 15) / 16));
+    smem = L.stage_off + (size_t)groups * f64_stage_doubles<DM, 5>() * sizeof(double);
+  }
   auto k = !LAT ? pnn_train_kernel<T, DM, HM, G, SC, PermT>
-                : (npw == 1 ? pnn_lat_kernel_shared<T, DM, 5, PermT>
-                            : npw == 2 ? pnn_lat_kernel_np2<T, DM, 5, PermT>
-                                       : pnn_lat_kernel<T, DM, 5, PermT>);
+                : F64 ? (npw == 1 ? (f64_short_minb() == 4 ? pnn_f64_kernel_shared4<DM, 5, PermT>
+                                                           : pnn_f64_kernel_shared<DM, 5, PermT>)
+                         : npw == 2 ? pnn_f64_kernel_np2<DM, 5, PermT>
+                                    : pnn_f64_kernel<DM, 5, PermT>)
+                      : (npw == 1 ? pnn_lat_kernel_shared<T, DM, 5, PermT>
+                                  : npw == 2 ? pnn_lat_kernel_np2<T, DM, 5, PermT>
+                                             : pnn_lat_kernel<T, DM, 5, PermT>);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -992,13 +1409,19 @@ static cudaError_t launch_variant(PnnLaunch L, int64_t nmax, size_t smem_limit, 
   return cudaGetLastError();
 }
 
+// uint16 in shared memory whenever one model's double buffer fits, else int32
+// in global memory.  The launcher's workspace allocation and the variant
+// choice both ask this one predicate (they must agree: the int32 variant
+// dereferences L.perm_global).
+static bool perm_fits_smem(int64_t nmax, size_t smem_limit) {
+  return nmax <= 65535 && pnn_smem_header(4, 4) + 2 * (size_t)nmax * sizeof(uint16_t) <= smem_limit;
+}
+
 template <typename T, int DM, int HM>
 static cudaError_t launch_dm_hm(const PnnLaunch& L, int64_t nmax, size_t smem_limit,
                                 cudaStream_t s) {
-  // uint16 in shared memory whenever one model's double buffer fits, else int32 in global
-  const bool fits = nmax <= 65535 &&
-                    pnn_smem_header(4, 4) + 2 * (size_t)nmax * sizeof(uint16_t) <= smem_limit;
-  if (fits) return launch_variant<T, DM, HM, uint16_t>(L, nmax, smem_limit, s);
+  if (perm_fits_smem(nmax, smem_limit)) return launch_variant<T, DM, HM, uint16_t>(L, nmax, smem_limit, s);
+  if (L.perm_global == nullptr) return cudaErrorInvalidValue;  // launcher invariant violated
   return launch_variant<T, DM, HM, int32_t>(L, nmax, smem_limit, s);
 }
 
@@ -1014,6 +1437,22 @@ static cudaError_t launch_bucket(int dm, int hm, const PnnLaunch& L, int64_t nma
   }
   return hm <= 16 ? launch_dm_hm<T, 16, 16>(L, nmax, smem_limit, s)
                   : launch_dm_hm<T, 16, 64>(L, nmax, smem_limit, s);
+}
+
+// {1 - 0.9^t, 1 - 0.999^t} for t = 1.. until both round to exactly 1.0,
+// with the host libm pow: the reference evaluates `1 - beta**t` with Python
+// float pow (pnn.py:185-186), i.e. the same C library call.
+static const std::vector<double2>& adam_bias_table() {
+  static const std::vector<double2> tab = [] {
+    std::vector<double2> v;
+    for (int t = 1;; ++t) {
+      const double a = 1.0 - std::pow(0.9, (double)t), b = 1.0 - std::pow(0.999, (double)t);
+      if (a == 1.0 && b == 1.0) break;
+      v.push_back(make_double2(a, b));
+    }
+    return v;
+  }();
+  return tab;
 }
 
 bbml_status pnn_train_launch(const bbml_pnn_task* tasks, int32_t n_tasks, const double* X,
@@ -1088,6 +1527,13 @@ bbml_status pnn_train_launch(const bbml_pnn_task* tasks, int32_t n_tasks, const 
     to_float_kernel<<<(int)std::min<int64_t>(ceil_div(rows, 256), 4096), 256, 0, stream>>>(
         X, x_stride, d_xf, xf_stride, y, d_yf, rows);
   }
+  // FP64: Adam bias-correction table (see pnn_f64_body)
+  double2* d_bc = nullptr;
+  const std::vector<double2>& bc_host = adam_bias_table();
+  if (precision == 64) {
+    if ((st = scratch.alloc(&d_bc, (int64_t)bc_host.size())) != BBML_OK) return st;
+    if ((st = scratch.upload(d_bc, bc_host.data(), (int64_t)bc_host.size())) != BBML_OK) return st;
+  }
   // shape groups (homogeneous launches); all scratch is allocated before the fork
   std::vector<std::pair<int, int>> groups_rng;
   int32_t* d_perm = nullptr;  // global double-buffer workspace, only if some bucket needs it
@@ -1100,8 +1546,7 @@ bbml_status pnn_train_launch(const bbml_pnn_task* tasks, int32_t n_tasks, const 
       nmax = std::max<int64_t>(nmax, sorted[b1].n);
       ++b1;
     }
-    const size_t elem = nmax <= 65535 ? 2 : 4;
-    if (2 * (size_t)nmax * elem + 1024 > smem_limit && d_perm == nullptr) {
+    if (!perm_fits_smem(nmax, smem_limit) && d_perm == nullptr) {
       if ((st = scratch.alloc(&d_perm, 2 * total)) != BBML_OK) return st;
     }
     groups_rng.push_back({b0, b1});
@@ -1130,6 +1575,9 @@ bbml_status pnn_train_launch(const bbml_pnn_task* tasks, int32_t n_tasks, const 
     L.history = history;
     L.status = status;
     L.perm_global = d_perm;
+    L.poll_cap_ns = precision == 64 ? 2000 : 100;
+    L.bc = d_bc;
+    L.bc_len = precision == 64 ? (int32_t)bc_host.size() : 0;
     cudaError_t e = precision == 32 ? launch_bucket<float>(dm, hm, L, nmax, smem_limit, stream)
                                     : launch_bucket<double>(dm, hm, L, nmax, smem_limit, stream);
     if (e != cudaSuccess) return cuda_status(e, "pnn_train launch");

@@ -90,6 +90,10 @@ bbml_status predict_launch(const bbml_pred_task* tasks, int32_t n_tasks, const d
       set_error("predict task %d: invalid field", i);
       return BBML_ERR_INVALID;
     }
+    if (t.d > x_stride) {  // the query rows must carry every input the model reads
+      set_error("predict task %d: d=%d exceeds the query row stride %d", i, t.d, x_stride);
+      return BBML_ERR_INVALID;
+    }
     if (t.norm_offset >= 0 && norm == nullptr) {
       set_error("predict task %d: normalizer requested but norm == NULL", i);
       return BBML_ERR_INVALID;

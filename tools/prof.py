@@ -17,7 +17,7 @@ ap.add_argument("--only-long", action="store_true")
 ap.add_argument("--top", type=int, default=0)
 ap.add_argument("--app", default=None)
 ap.add_argument("--br-epochs", type=int, default=1000)
-ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--reps", type=int, default=3)
 a = ap.parse_args()
 series, spec, kw = bench.workload_series(a.workload)
 if a.only_long:
@@ -39,7 +39,7 @@ def timed(fn):
 res = {}
 for rep in range(a.reps):
     if len(wl.pnn):
-        res["pnn_ms"] = timed(lambda: check(so.bbml_pnn_train(ptr(dev.pnn_tab), len(dev.pnn_tab), ptr(dev.X), ptr(dev.y), wl.train.stride, ptr(dev.weights), None, ptr(dev.status), wl.precision, s.cuda_stream), "pnn"))
+        res["pnn_ms"] = min(res.get("pnn_ms", 1e30), timed(lambda: check(so.bbml_pnn_train(ptr(dev.pnn_tab), len(dev.pnn_tab), ptr(dev.X), ptr(dev.y), wl.train.stride, ptr(dev.weights), None, ptr(dev.status), wl.precision, s.cuda_stream), "pnn")))
     if len(wl.lm):
         off = 8 * int(wl.P_pnn.sum())
         res["lm_ms"] = timed(lambda: check(so.bbml_lm_train(ptr(dev.lm_tab), len(dev.lm_tab), ptr(dev.X), ptr(dev.y), wl.train.stride, ptr(dev.weights) + off, None, ptr(dev.status) + STATUS.itemsize * len(wl.pnn), s.cuda_stream), "lm"))

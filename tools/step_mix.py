@@ -9,7 +9,7 @@ import bench
 
 R = int(os.environ.get("R", "32"))
 series, spec, kw = bench.workload_series("suite16")
-wl = batch.build_workload(series, spec, restarts=list(range(R)), precision=32, **kw)
+wl = batch.build_workload(series, spec, restarts=list(range(R)), precision=int(os.environ.get("PREC", "32")), **kw)
 dev = batch.DeviceWorkload(wl)
 papp = np.array([wl.keys[i][0] for i in wl.pnn_series])
 lapp = np.array([wl.keys[i][0] for i in wl.lm_series])
