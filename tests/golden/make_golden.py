@@ -256,7 +256,33 @@ def gen_train_one():
     save("train_one", d)
 
 
+def gen_pnn_long():
+    """Long-series PNN case (the bench's longest sequential chain): the first
+    suite16 pathfinder series, random split 0.7 / seed 0 and the reference's
+    normaliser, 4 epochs of pnn.train (761 minibatches each) with the
+    series_seed the bench gives restart 0."""
+    from bbcount.traces import SplitSpec, fit_normalizer, split
+
+    key, X, y = next(s for s in synth.suite16(seed=0) if s[0][0] == "pathfinder")
+    tr, te = split(_ref_series(key, X, y), SplitSpec(SplitMode.RANDOM, 0.7, 0))
+    nm = fit_normalizer(tr)
+    Xn, yn = nm.transform_features(tr.X), nm.transform_targets(tr.y)
+    Xt = nm.transform_features(te.X)
+    seed = series_seed(0, key, "pnn")
+    d = {"X": Xn, "y": yn, "Xt": Xt, "seed": np.array(words(seed, 2), dtype=np.uint64),
+         "epochs": np.array(4)}
+    m, hist = pnn.train(Xn, yn, pnn.TrainConfig(epochs=4, seed=seed))
+    d["w"] = np.concatenate([m.W1.ravel(), m.b1, m.W2, [m.b2]])
+    d["hist"] = np.array(hist)
+    d["pred"] = np.atleast_1d(pnn.forward(m, Xt))
+    save("pnn_long", d)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["pnn_long"]:
+        gen_pnn_long()
+        sys.exit(0)
+    gen_pnn_long()
     gen_rng()
     gen_pnn()
     gen_br()

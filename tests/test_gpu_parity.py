@@ -75,6 +75,26 @@ def test_pnn_fp32_predictions_within_gate(golden):
         pnn.PRECISION = old
 
 
+def test_pnn_long_series_matches_reference_golden(golden):
+    """Pathfinder-size PNN (7,604 rows: the long-series kernel with one
+    producer warp per model, the uint16 permutation double buffer at its
+    largest and the epoch-boundary stream rewind) against the reference's own
+    run: FP64 history <= 1e-12, weights <= 1e-11; FP32 predictions <= 1e-3."""
+    g = golden("pnn_long")
+    cfg = pnn.TrainConfig(epochs=int(g["epochs"]), seed=_seed(g["seed"]))
+    model, hist = pnn.train(g["X"], g["y"], cfg)
+    assert _rel(hist, g["hist"]) <= 1e-12, _rel(hist, g["hist"])
+    assert _rel(model.packed(), g["w"]) <= 1e-11, _rel(model.packed(), g["w"])
+    assert _rel(pnn.forward(model, g["Xt"]), g["pred"]) <= 1e-11
+    old = pnn.PRECISION
+    pnn.PRECISION = 32
+    try:
+        m32, _ = pnn.train(g["X"], g["y"], cfg)
+    finally:
+        pnn.PRECISION = old
+    assert _rel(pnn.forward(m32, g["Xt"]), g["pred"]) <= 1e-3
+
+
 def test_br_matches_reference_golden(golden):
     g = golden("brbpnn")
     worst = {}
@@ -172,28 +192,48 @@ def test_br_wide_first_epoch_and_gamma_within_reference_self_spread():
         assert lo <= r_d.gamma <= hi, (d, h, n, r_d.gamma, env, spread)
 
 
-def test_br_hidden10_accuracy_parity_gramschmit():
-    """Accuracy parity (north-star gate, +-0.5 pp) for the near-chaotic h = 10
-    models: the 83 gramschmit series of suite16, random split, 200 epochs."""
+def _spread_gate(label, items, data, kw, oracle_pred, floors):
+    """For fits beyond 1e-3: device error <= 25 x the oracle's own 1-ulp
+    spread (oracle.pool.self_spread), which must itself exceed 1e-3 / 25."""
+    from oracle.pool import self_spread
+
+    for key, e in items:
+        X, y = data[key]
+        spread = self_spread(key, X, y, "brbpnn", kw, oracle_pred[key], floors[key])
+        print(f"{label} {key}: device {e:.2e}, oracle 1-ulp spread {spread:.2e}")
+        assert spread * 25 >= 1e-3 and e <= 25 * spread, (key, e, spread)
+
+
+def test_br_hidden10_parity_gramschmit_1000_epochs():
+    """The near-chaotic hidden-10 fits (the 83 gramschmit series of suite16,
+    random split, the bench's 1000 epochs) through the drop-in
+    experiment.train_many: predicted counts <= max(1e-3, 25 x the oracle's
+    own 1-ulp spread) per series, accuracy within +-0.5 pp."""
     from paper_2202_07798_b200 import synth
     from paper_2202_07798_b200.experiment import ExperimentConfig, train_many
     from paper_2202_07798_b200.traces import BbSeries, SplitMode
+    from oracle.pool import oracle_map, rel
 
     raw = [s for s in synth.suite16(seed=0) if s[0][0] == "gramschmit"]
     series = [BbSeries(k, X, y) for k, X, y in raw]
-    cfg = ExperimentConfig(split_mode=SplitMode.RANDOM, seed=0, br_hidden=10, br_max_epochs=200,
+    cfg = ExperimentConfig(split_mode=SplitMode.RANDOM, seed=0, br_hidden=10, br_max_epochs=1000,
                            models=("brbpnn",))
     res = train_many([(s, "brbpnn") for s in series], cfg).results
-    dev = [r.mse for r in res if r.error is None]
-    ora = []
-    for k, X, y in raw:
-        r = O.train_one(k, X, y, "brbpnn", mode="random", base_seed=0, br_hidden=10, br_max_epochs=200)
-        if r.error is None:
-            ora.append(r.mse)
-    assert len(dev) == len(ora) == len(series)
-    acc_dev = 100 * (1 - float(np.mean(dev)))
-    acc_ora = 100 * (1 - float(np.mean(ora)))
-    print("gramschmit h=10 accuracy device %.3f oracle %.3f" % (acc_dev, acc_ora))
+    kw = dict(mode="random", base_seed=0, br_hidden=10, br_max_epochs=1000)
+    ora = oracle_map([(k, X, y, "brbpnn", kw, None) for k, X, y in raw])
+    floors = {k: 1e-6 * max(1.0, float(np.max(np.abs(y)))) for k, X, y in raw}
+    beyond = []
+    for (k, X, y), r, o in zip(raw, res, ora):
+        assert r.error is None and o.error is None, (k, r.error, o.error)
+        e = rel(r.pred_raw, o.pred_raw, floors[k])
+        if e > 1e-3:
+            beyond.append((k, e))
+    by = {k: (X, y) for k, X, y in raw}
+    _spread_gate("gramschmit h=10", beyond, by, kw, {k: o.pred_raw for (k, _, _), o in zip(raw, ora)},
+                 floors)
+    acc_dev = 100 * (1 - float(np.mean([r.mse for r in res])))
+    acc_ora = 100 * (1 - float(np.mean([o.mse for o in ora])))
+    print("gramschmit h=10 accuracy device %.3f oracle %.3f, beyond 1e-3: %d" % (acc_dev, acc_ora, len(beyond)))
     assert abs(acc_dev - acc_ora) <= 0.5
 
 
@@ -239,13 +279,22 @@ def test_train_one_matches_reference_golden(golden):
             # relative error with a floor at 1e-6 of the series' count scale
             # (predictions of a count that is 0 on the test side are ~1e-9)
             floor = 1e-6 * max(1.0, float(np.max(np.abs(g[p + "y"]))))
-            if kind == "brbpnn" and float(g[p + "br_meta"][4]) >= 1e12:
+            e = _rel(r.pred_raw, g[p + "pred_raw"], floor)
+            if kind == "brbpnn" and float(g[p + "br_meta"][4]) >= 1e12 and e > tol:
                 # degenerate fit: E_D -> 0 drives beta to its 1e12 clamp and the
                 # damped system to condition ~1e24, so late epochs amplify
-                # rounding (a step target fitted by a saturating tanh).  Gate on
-                # accuracy parity (north star: +-0.5 pp) instead of 1e-3.
-                assert abs(r.mse - float(g[p + "mse"])) <= 0.005, (key, kind)
-                assert _rel(r.pred_raw, g[p + "pred_raw"], floor) <= 1e-2, (key, kind)
+                # rounding (a step target fitted by a saturating tanh).  Gate
+                # at max(1e-3, 25 x the reference's own 1-ulp spread), the
+                # spread measured here by re-running the oracle (bit-identical
+                # to the reference) on its normalised training data moved by
+                # one ulp (oracle.PERTURBATIONS).
+                from oracle.pool import self_spread
+
+                spread = self_spread(key, g[p + "X"], g[p + "y"], kind,
+                                     dict(mode=mode, base_seed=seed, pnn_epochs=pe, br_max_epochs=be),
+                                     g[p + "pred_raw"], floor)
+                print(f"beta-clamped {key}: device {e:.2e}, reference 1-ulp spread {spread:.2e}")
+                assert e <= max(1e-3, 25 * spread), (key, kind, e, spread)
                 checked += 1
                 continue
             assert _rel(r.pred_raw, g[p + "pred_raw"], floor) <= tol, (key, kind)
@@ -302,34 +351,39 @@ def test_learning_curves_batched_match_oracle(tmp_path):
     assert len(list(tmp_path.glob("curve_*.csv"))) == 6
 
 
-def test_br_wide_accuracy_parity_hidden64():
-    """BASELINE cfg 5 (hidden 64, P = 257) on the device's wide path: accuracy
-    parity with the oracle within the north-star +-0.5 pp over ten app20
-    series (HighLow split, 100 training rows, 60 LM epochs), plus per-series
-    agreement of the test MSE within 0.05 (the trajectories are near-chaotic,
-    SURVEY §8c)."""
+def test_br_wide_parity_hidden64_1000_epochs():
+    """BASELINE cfg 5 (hidden 64, P = 257) on the device's wide path at the
+    bench's 1000 epochs, ten app20 series (HighLow split, 100 training rows):
+    predicted counts <= max(1e-3, 25 x the oracle's own 1-ulp spread) per
+    series, accuracy within the north-star +-0.5 pp."""
     from paper_2202_07798_b200 import synth
     from paper_2202_07798_b200.experiment import ExperimentConfig, train_many
     from paper_2202_07798_b200.traces import BbSeries, SplitMode
+    from oracle.pool import oracle_map, rel
 
     raw = synth.app20()[:10]
     series = [BbSeries(k, X, y) for k, X, y in raw]
-    cfg = ExperimentConfig(split_mode=SplitMode.HIGH_LOW, seed=0, br_hidden=64, br_max_epochs=60,
+    cfg = ExperimentConfig(split_mode=SplitMode.HIGH_LOW, seed=0, br_hidden=64, br_max_epochs=1000,
                            models=("brbpnn",))
     res = train_many([(s, "brbpnn") for s in series], cfg).results
-    dev, ora = [], []
-    for (k, X, y), r in zip(raw, res):
-        o = O.train_one(k, X, y, "brbpnn", mode="high-low", base_seed=0, br_hidden=64,
-                        br_max_epochs=60)
+    kw = dict(mode="high-low", base_seed=0, br_hidden=64, br_max_epochs=1000)
+    ora = oracle_map([(k, X, y, "brbpnn", kw, None) for k, X, y in raw])
+    floors = {k: 1e-6 * max(1.0, float(np.max(np.abs(y)))) for k, X, y in raw}
+    dev, orc, beyond = [], [], []
+    for (k, X, y), r, o in zip(raw, res, ora):
         assert (r.error is None) == (o.error is None), (k, r.error, o.error)
         if r.error is None:
             dev.append(r.mse)
-            ora.append(o.mse)
-            assert abs(r.mse - o.mse) <= 0.05, (k, r.mse, o.mse)
+            orc.append(o.mse)
+            e = rel(r.pred_raw, o.pred_raw, floors[k])
+            if e > 1e-3:
+                beyond.append((k, e))
     assert len(dev) >= 8
+    by = {k: (X, y) for k, X, y in raw}
+    _spread_gate("hidden 64", beyond, by, kw, {k: o.pred_raw for (k, _, _), o in zip(raw, ora)}, floors)
     acc_dev = 100 * (1 - float(np.mean(dev)))
-    acc_ora = 100 * (1 - float(np.mean(ora)))
-    print("hidden-64 accuracy device %.3f oracle %.3f" % (acc_dev, acc_ora))
+    acc_ora = 100 * (1 - float(np.mean(orc)))
+    print("hidden-64 accuracy device %.3f oracle %.3f, beyond 1e-3: %d" % (acc_dev, acc_ora, len(beyond)))
     assert abs(acc_dev - acc_ora) <= 0.5
 
 
@@ -337,8 +391,8 @@ def test_br_hidden1_long_series_multiwarp():
     """Hidden-1 fits with n >= 2048 training rows run one model per CTA of 4
     warps (sample passes split over warps, reduced in warp order); against
     the oracle's train_one on the same random split: predictions <= 1e-6
-    relative (accuracy gate for a beta-clamped degenerate fit, as in
-    test_train_one_matches_reference_golden)."""
+    relative, or max(1e-3, 25 x the oracle's own 1-ulp spread) for a
+    beta-clamped degenerate fit (as in test_train_one_matches_reference_golden)."""
     from paper_2202_07798_b200 import synth
     from paper_2202_07798_b200.experiment import ExperimentConfig, train_many
     from paper_2202_07798_b200.traces import BbSeries, SplitMode
@@ -353,9 +407,16 @@ def test_br_hidden1_long_series_multiwarp():
         assert r.error is None and o.error is None, (k, r.error, o.error)
         assert r.n_train == o.n_train and r.n_train >= 2048
         floor = 1e-6 * max(1.0, float(np.max(np.abs(y))))
-        if abs(r.mse - o.mse) <= 1e-12 or _rel(r.pred_raw, o.pred_raw, floor) <= 1e-6:
+        e = _rel(r.pred_raw, o.pred_raw, floor)
+        if e <= 1e-6:
             continue
-        assert abs(r.mse - o.mse) <= 0.005, (k, r.mse, o.mse)
+        # beyond 1e-6: max(1e-3, 25 x the oracle's own 1-ulp spread)
+        from oracle.pool import self_spread
+
+        spread = self_spread(k, X, y, "brbpnn", dict(mode="random", base_seed=1, br_max_epochs=300),
+                             o.pred_raw, floor)
+        print(f"multi-warp {k}: device {e:.2e}, oracle 1-ulp spread {spread:.2e}")
+        assert e <= max(1e-3, 25 * spread), (k, e, spread)
 
 
 def test_device_metrics_match_metrics_py():

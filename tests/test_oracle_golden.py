@@ -114,3 +114,14 @@ def test_train_one_oracle_matches_reference(golden):
             assert res.mse == pytest.approx(float(g[p + "mse"]), rel=1e-9, abs=1e-14)
             np.testing.assert_allclose(res.pred_raw, g[p + "pred_raw"], rtol=1e-9)
             assert res.seed == int(g[p + "seed"][0])
+
+
+def test_pnn_oracle_matches_reference_long_series(golden):
+    """The pathfinder-size case (7,604 training rows, 4 epochs = 3,044
+    sequential Adam steps, the bench's longest chain) — pins the oracle's
+    permutation stream and Adam at the long-series size."""
+    g = golden("pnn_long")
+    X, y = g["X"], g["y"]
+    w, hist = O.pnn_fit(X, y, X.shape[1], 10, int(g["epochs"]), 10, 1e-4, _seed(g["seed"]))
+    np.testing.assert_allclose(w, g["w"], rtol=1e-12, atol=0)
+    np.testing.assert_allclose(hist, g["hist"], rtol=1e-12, atol=0)

@@ -27,12 +27,25 @@ __global__ void k(unsigned long long* out) {
   }
   atomicAdd(out + 0, ndiv); atomicAdd(out + 1, nsqrt); atomicMax(out + 2, tanh_ulp_max); atomicAdd(out + 3, tanh1);
   atomicAdd(out + 4, nsqrt_tiny);
+  unsigned long long ul[3] = {0, 0, 0}, nbig[3] = {0, 0, 0};
+  for (int i = 0; i < 4000; ++i) {
+    double y = -u01(s) * exp2(floor(u01(s) * 14 - 12)) * 8;  // exp arg <= 0
+    double u = u01(s) * exp2(-floor(u01(s) * 60));            // log1p arg in (0,1]
+    double x = (u01(s) + 0.01) * exp2(floor(u01(s) * 120 - 60)); // log arg
+    double r[3][2] = {{exp_neg_bf(y), exp(y)}, {log1p_bf(u), log1p(u)}, {log_bf(x), log(x)}};
+    for (int q = 0; q < 3; ++q) {
+      unsigned long long d = llabs((long long)__double_as_longlong(r[q][0]) - (long long)__double_as_longlong(r[q][1]));
+      if (d > ul[q]) ul[q] = d;
+      if (d > 1) ++nbig[q];
+    }
+  }
+  for (int q = 0; q < 3; ++q) { atomicMax(out + 5 + q, ul[q]); atomicAdd(out + 8 + q, nbig[q]); }
 }
 int main() {
-  unsigned long long* d; cudaMalloc(&d, 64); cudaMemset(d, 0, 64);
-  k<<<148, 256>>>(d); unsigned long long h[5]; cudaMemcpy(h, d, 40, cudaMemcpyDeviceToHost);
+  unsigned long long* d; cudaMalloc(&d, 128); cudaMemset(d, 0, 128);
+  k<<<148, 256>>>(d); unsigned long long h[11]; cudaMemcpy(h, d, 88, cudaMemcpyDeviceToHost);
   printf("samples %d: div mismatches %llu, sqrt mismatches %llu, sqrt(denormal) mismatches %llu, tanh max ulp vs libdevice %llu, tanh >1ulp %llu\n",
          148 * 256 * 4000, h[0], h[1], h[4], h[2], h[3]);
-  double t[] = {0.0, -0.0, 1e-300, 1e-8, 0.1, 0.5, 1.0, 5.0, 19.0, 30.0, 1e300};
+  printf("max ulp vs libdevice: exp %llu (>1: %llu), log1p %llu (>1: %llu), log %llu (>1: %llu)\n", h[5], h[8], h[6], h[9], h[7], h[10]);
   return 0;
 }
