@@ -23,7 +23,8 @@ import numpy as np
 
 from . import _lib, engine
 from ._lib import PRED_TASK, STATUS, check, lib, ptr
-from .traces import BbSeries, SplitSpec, split, fit_normalizer, SplitError
+from . import prep
+from .traces import BbSeries, Normalizer, SplitSpec
 
 
 @dataclass
@@ -48,6 +49,8 @@ class Workload:
 
     def norm_rows(self) -> np.ndarray:
         """(series, 2*d_max+2) rows of [x_min(d), x_max(d), y_min, y_max]."""
+        if getattr(self, "_norm_rows", None) is not None:
+            return self._norm_rows
         dmax = max([int(self.train.d.max()) if len(self.train.d) else 1, 1])
         rows = np.zeros((len(self.keys), 2 * dmax + 2))
         for i, nm in enumerate(self.norms):
@@ -82,35 +85,25 @@ class Workload:
 def build_workload(series: Sequence[BbSeries], spec: SplitSpec, *, kinds=("pnn", "brbpnn"),
                    restarts: Sequence[int] = (0,), pnn_epochs=300, pnn_batch=10, pnn_lr=1e-4,
                    pnn_hidden=10, br_hidden: int | Callable = 1, br_max_epochs=1000,
-                   precision=64) -> Workload:
-    """Split + normalise every series once (traces.py semantics), then one
-    PNN and/or BR task per (series, restart); restart r seeds the model with
+                   precision=64, table: Optional[prep.SeriesTable] = None) -> Workload:
+    """Split + normalise every series once (``prep.prepare``: whole-array
+    passes with the reference's traces.py semantics), then one PNN and/or BR
+    task per (series, restart); restart r seeds the model with
     experiment.series_seed(r, key, kind)."""
-    keys, norms, Xtr, ytr, Xte, yte, errors, yraw = [], [], [], [], [], [], {}, []
-    for s in series:
-        try:
-            tr, te = split(s, spec)
-        except SplitError as exc:
-            errors[len(keys)] = str(exc)
-            keys.append(s.key)
-            norms.append(None)
-            for lst in (Xtr, Xte):
-                lst.append(np.zeros((0, s.arity)))
-            ytr.append(np.zeros(0))
-            yte.append(np.zeros(0))
-            yraw.append(np.zeros(0))
-            continue
-        nm = fit_normalizer(tr)
-        keys.append(s.key)
-        norms.append(nm)
-        Xtr.append(nm.transform_features(tr.X))
-        ytr.append(nm.transform_targets(tr.y))
-        Xte.append(nm.transform_features(te.X))
-        yte.append(nm.transform_targets(te.y))
-        yraw.append(np.asarray(te.y, dtype=np.float64))
-    train = engine.pack(Xtr, ytr)
-    test = engine.pack(Xte, yte)
-    ok = np.array([i for i in range(len(keys)) if i not in errors], dtype=np.int64)
+    t = prep.SeriesTable.from_series(series) if table is None else table
+    P = prep.prepare(t, spec.mode.value, spec.fraction, spec.seed)
+    keys = list(t.keys)
+    S = len(keys)
+    dmax = t.X.shape[1]
+    ok_mask = np.zeros(S, dtype=bool)
+    ok_mask[P.ok] = True
+    d_ser = np.where(ok_mask, t.d, 0).astype(np.int32)
+    train = engine.Packed(P.Xtr, P.ytr, P.tr_off[:-1].copy(), np.diff(P.tr_off).astype(np.int32), t.d.copy())
+    test = engine.Packed(P.Xte, P.yte, P.te_off[:-1].copy(), np.diff(P.te_off).astype(np.int32), t.d.copy())
+    norms = [None if not ok_mask[i] else
+             Normalizer(P.x_min[i, :t.d[i]].copy(), P.x_max[i, :t.d[i]].copy(), float(P.y_min[i]),
+                        float(P.y_max[i])) for i in range(S)]
+    ok = P.ok.astype(np.int64)
     app_crc = np.array([zlib.crc32(k[0].encode("utf-8")) for k in keys], dtype=np.uint64)
     kid = np.array([k[1] for k in keys], dtype=np.uint64)
     bid = np.array([k[2] for k in keys], dtype=np.uint64)
@@ -127,24 +120,25 @@ def build_workload(series: Sequence[BbSeries], spec: SplitSpec, *, kinds=("pnn",
             sidx.append(ok)
         seeds = np.concatenate(seeds)
         sidx = np.concatenate(sidx)
-        rb, n, d = train.row_begin[sidx], train.n[sidx], train.d[sidx]
+        rb, n, d = train.row_begin[sidx], train.n[sidx], d_ser[sidx]
         if kind == "pnn":
-            tab, P = engine.pnn_tasks(rb, n, d, pnn_hidden, pnn_epochs, pnn_batch, pnn_lr, 1e-8,
-                                      seeds, False)
+            tab, Pn = engine.pnn_tasks(rb, n, d, pnn_hidden, pnn_epochs, pnn_batch, pnn_lr, 1e-8,
+                                       seeds, False)
         else:
             h = (np.array([br_hidden(keys[i]) for i in sidx], dtype=np.int32)
                  if callable(br_hidden) else br_hidden)
-            tab, P = engine.lm_tasks(rb, n, d, h, br_max_epochs, seeds, False)
-        tabs[kind] = (tab, P, sidx)
+            tab, Pn = engine.lm_tasks(rb, n, d, h, br_max_epochs, seeds, False)
+        tabs[kind] = (tab, Pn, sidx)
     empty_p = np.zeros(0, dtype=_lib.PNN_TASK)
     empty_l = np.zeros(0, dtype=_lib.LM_TASK)
     pt, pP, ps = tabs["pnn"]
     lt, lP, ls = tabs["brbpnn"]
-    return Workload(train, test, keys, norms, empty_p if pt is None else pt,
-                    empty_l if lt is None else lt, ps, ls,
-                    np.zeros(0, np.int64) if pt is None else pP,
-                    np.zeros(0, np.int64) if lt is None else lP, precision, errors,
-                    np.concatenate(yraw) if yraw else np.zeros(0))
+    wl = Workload(train, test, keys, norms, empty_p if pt is None else pt,
+                  empty_l if lt is None else lt, ps, ls,
+                  np.zeros(0, np.int64) if pt is None else pP,
+                  np.zeros(0, np.int64) if lt is None else lP, precision, P.errors, P.yte_raw)
+    wl._norm_rows = P.norm_rows(dmax)
+    return wl
 
 
 class DeviceWorkload:

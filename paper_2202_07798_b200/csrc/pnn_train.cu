@@ -1095,14 +1095,13 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
       const bool mine = j < SP && (sg * SP + j) < cnt;
       const double nb_t = (double)nb;
       const double zz = __dadd_rn(zj, b2);
-      const double sp = softplus(zz);
+      // softplus = numpy logaddexp(0, z) = max(z, 0) + log1p(exp(-|z|))
+      const double sp = __dadd_rn(fmax(zz, 0.0), log1p_bf(exp_neg_bf(-fabs(zz))));
       const double rate = __dadd_rn(sp, eps);
       const double re = __dadd_rn(rate, eps);
-      // y == 0 (the series minimum after normalisation): 0 / re == 0 exactly,
-      // without the division's special-operand path
       const double drate = div_rn_bf(__dsub_rn(1.0, div_rn_bf(yj, re)), nb_t);
-      const double dzj = mine ? __dmul_rn(drate, exp(__dsub_rn(zz, sp))) : 0.0;
-      if (mine) bloss += __dsub_rn(rate, __dmul_rn(yj, log(re)));
+      const double dzj = mine ? __dmul_rn(drate, exp_neg_bf(__dsub_rn(zz, sp))) : 0.0;
+      if (mine) bloss += __dsub_rn(rate, __dmul_rn(yj, log_bf(re)));
       // backward (pnn.py:139-146)
 #pragma unroll
       for (int i = 0; i < SP; ++i) {

@@ -25,7 +25,7 @@ from typing import Optional, Sequence, Union
 
 import numpy as np
 
-from . import __version__, _lib, brbpnn, engine, metrics, pnn
+from . import __version__, _lib, brbpnn, engine, metrics, pnn, prep
 from .persist import SavedModel, save_model
 from .traces import (BbSeries, Normalizer, SplitError, SplitMode, SplitSpec, classify,
                      fit_normalizer, split, trace_header)
@@ -104,14 +104,29 @@ class Prepared:
 
 
 def prepare(series: BbSeries, spec: SplitSpec) -> Prepared:
-    """experiment.py:105-116: split, fit the normaliser on train, transform."""
-    try:
-        tr, te = split(series, spec)
-    except SplitError as exc:
-        return Prepared(series, error=str(exc))
-    norm = fit_normalizer(tr)
-    return Prepared(series, None, norm, norm.transform_features(tr.X), norm.transform_targets(tr.y),
-                    norm.transform_features(te.X), norm.transform_targets(te.y), te.y)
+    """experiment.py:105-116 for one series: split, fit the normaliser on
+    train, transform (one-series case of ``prepare_many``)."""
+    return prepare_many([series], spec)[0]
+
+
+def prepare_many(series_list: Sequence[BbSeries], spec: SplitSpec) -> list:
+    """Split + normalise many series in whole-array passes (``prep.prepare``)
+    and hand back per-series views."""
+    table = prep.SeriesTable.from_series(series_list)
+    P = prep.prepare(table, spec.mode.value, spec.fraction, spec.seed)
+    out = []
+    for i, s in enumerate(series_list):
+        if i in P.errors:
+            out.append(Prepared(s, error=P.errors[i]))
+            continue
+        d = int(table.d[i])
+        a, b = int(P.tr_off[i]), int(P.tr_off[i + 1])
+        c, e = int(P.te_off[i]), int(P.te_off[i + 1])
+        norm = Normalizer(P.x_min[i, :d].copy(), P.x_max[i, :d].copy(), float(P.y_min[i]),
+                          float(P.y_max[i]))
+        out.append(Prepared(s, None, norm, P.Xtr[a:b, :d], P.ytr[a:b], P.Xte[c:e, :d], P.yte[c:e],
+                            P.yte_raw[c:e]))
+    return out
 
 
 @dataclass
@@ -181,16 +196,25 @@ def train_many(pairs: Sequence[tuple], config: ExperimentConfig, *, precision: O
     results: list = [None] * len(pairs)
     tasks: dict = {"pnn": [], "brbpnn": []}
     order: dict = {"pnn": [], "brbpnn": []}
+    def cache_key(series, sp):
+        return id(series) if sp is spec else (id(series), sp.mode, sp.fraction, sp.seed)
+
+    # batched split + normalise of every (series, split) not prepared yet
+    todo: dict = {}
+    for pair in pairs:
+        sp = pair[2] if len(pair) > 2 else spec
+        ck = cache_key(pair[0], sp)
+        if ck not in cache:
+            todo.setdefault((sp.mode, sp.fraction, sp.seed), {})[ck] = pair[0]
+    for (mode, fraction, seed), group in todo.items():
+        for ck, p in zip(group, prepare_many(list(group.values()), SplitSpec(mode, fraction, seed))):
+            cache[ck] = p
     for i, pair in enumerate(pairs):
         series, kind = pair[0], pair[1]
         sp = pair[2] if len(pair) > 2 else spec
         res = SeriesResult(series.key, kind)
         results[i] = res
-        ck = id(series) if sp is spec else (id(series), sp.mode, sp.fraction, sp.seed)
-        p = cache.get(ck)
-        if p is None:
-            p = prepare(series, sp)
-            cache[ck] = p
+        p = cache[cache_key(series, sp)]
         if p.error is not None:
             res.error = p.error
             continue
