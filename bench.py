@@ -1,19 +1,31 @@
 """Benchmark: models trained/sec for BB-ML's PNN + BR-BPNN on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload suite16]
-                    [--restarts R] [--precision 32|64] [--impl ours|reference]
+                    [--restarts R] [--precision 64|32] [--scaling weak|strong]
+                    [--impl ours|reference]
 
 One step = train every model of the workload from scratch (PNN and BR-BPNN,
-one fused kernel each, concurrently), predict every model's test rows and
-compute every model's test MSE / Pearson / Spearman on the device.
-Inputs (CSR-packed, normalised training/test rows) are resident in HBM for
-`value`; `e2e` times the public batched call (batch.fit_predict path) with
-H2D from pinned host buffers and D2H of weights / status / per-model test
-metrics (computed on the device from the predictions) each step.
-Multi-GPU (torchrun): every rank trains its own restarts of the workload
-(weak scaling, no data-path collective); time = max over ranks.
-`--impl reference` times the CPU oracle port (numpy restatement of the
-reference, bit-identical to it) on the host cores with a process pool.
+one fused kernel call each, concurrently), predict every model's test rows
+and compute every model's test MSE / Pearson / Spearman on the device.
+The headline arithmetic is FP64 (the reference's and the drop-in's);
+``--precision 32`` runs the PNN fits in FP32 (BR-BPNN is FP64 always).
+
+``value``: device-timed steps with the prepared inputs resident in HBM.
+``e2e``: the public path a user runs, every step: raw series rows (host) ->
+batched split + normalise + task tables (``batch.build_workload``) -> pinned
+staging -> H2D -> train / predict / metrics -> D2H of weights, statuses and
+per-model metrics.
+Multi-GPU (torchrun, one process per GPU):
+  weak   (default) every rank trains its own restarts of the workload;
+  strong  the fixed unit list (series x restarts) is LPT-sharded over the
+          ranks and every step ends with an all-gather of every model's
+          status / metrics / weights in task order (sharding.py) — the only
+          collective.  Time = max over ranks.
+``--impl reference`` (and ``cpu_baseline``) time the CPU oracle port
+(oracle/bbml_oracle.py, bit-identical to the reference on its golden
+vectors) on the host cores: every task of restart 0 of the workload through
+a process pool, plus the serial and GIL-thread (the reference's
+``run_experiment(workers=...)``) modes.
 """
 
 from __future__ import annotations
@@ -42,19 +54,21 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--workload", default="suite16", choices=WORKLOADS)
     ap.add_argument("--restarts", type=int, default=None)
-    ap.add_argument("--precision", type=int, default=32, choices=(32, 64))
+    ap.add_argument("--precision", type=int, default=64, choices=(32, 64))
+    ap.add_argument("--scaling", default="weak", choices=("weak", "strong"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=None)
+    ap.add_argument("--cpu-sample", type=int, default=None,
+                    help="CPU legs: a stratified subset of this many tasks instead of all (tests)")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
 
 
-# restarts per GPU: suite16 32 (fills the GPU), sweep 16 (SURVEY §8d cfg 4), wide 7
-# (140 CTA-per-model BR-BPNN fits on 148 SMs)
+# restarts per GPU (weak) or in total (strong): suite16 32 (fills one GPU),
+# sweep 16 (SURVEY §8d cfg 4), wide 7 (140 CTA-per-model fits on 148 SMs)
 DEFAULT_RESTARTS = {"suite16": 32, "app20": 1, "sweep": 16, "wide": 7}
 
 # BR-BPNN tasks at or above this hidden size are timed on the CPU for
-# CPU_EPOCH_SAMPLE epochs and extrapolated per epoch (a full h = 64 fit takes
+# CPU_EPOCH_SAMPLE epochs and scaled per epoch (a full h = 64 fit takes
 # minutes of CPU time); SURVEY §8d "time a sample and extrapolate"
 CPU_WIDE_HIDDEN = 32
 CPU_EPOCH_SAMPLE = 3
@@ -157,16 +171,26 @@ def measure_fma_peak(torch, precision):
 
 
 # ---------------------------------------------------------------------------
-# CPU side (oracle port) — the checker/baseline only
+# CPU side (oracle port) — the checker / baseline only
 # ---------------------------------------------------------------------------
 
-def _cpu_task(args):
-    """Seconds for one model on one core; wide BR fits are timed for
-    CPU_EPOCH_SAMPLE epochs and scaled to `full_epochs` epochs."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _cpu_task(job):
+    """(seconds, sampled) for one model on one core; wide BR fits are timed
+    for CPU_EPOCH_SAMPLE epochs and scaled to the epochs the device ran."""
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     from oracle import bbml_oracle as O
 
-    key, X, y, kind, mode, frac, base, br_hidden, full_epochs = args
+    key, X, y, kind, mode, frac, base, br_hidden, full_epochs = job
     sampled = kind == "brbpnn" and br_hidden >= CPU_WIDE_HIDDEN
     t0 = time.perf_counter()
     r = O.train_one(key, X, y, kind, mode=mode, fraction=frac, base_seed=base, br_hidden=br_hidden,
@@ -174,52 +198,80 @@ def _cpu_task(args):
     dt = time.perf_counter() - t0
     if sampled and r.epochs_run:
         dt *= full_epochs / r.epochs_run
-    return dt
-
-
-def cpu_sample_tasks(series, spec, wl_kw, restarts, sample, full_epochs=1000):
-    """Stratified sample: tasks ordered by a cost estimate, one pick per
-    equal-count stratum (median of the stratum)."""
-    kinds = wl_kw.get("kinds", ("pnn", "brbpnn"))
-    bh = wl_kw.get("br_hidden", 1)
-    tasks = []
-    for s in series:
-        n = len(s) * spec.fraction if spec.mode.value == "random" else len(s) * 0.5
-        for kind in kinds:
-            h = bh(s.key) if callable(bh) else bh
-            cost = n * (300.0 if kind == "pnn" else 20.0 * h * h)
-            tasks.append((cost, s, kind, h))
-    tasks.sort(key=lambda t: t[0])
-    S = min(sample, len(tasks))
-    picks = [tasks[int((i + 0.5) * len(tasks) / S)] for i in range(S)]
-    return [(s.key, s.X, s.y, kind, spec.mode.value, spec.fraction, r % max(restarts, 1), h,
-             full_epochs) for i, (_, s, kind, h) in enumerate(picks) for r in (i,)]
+    return dt, sampled
 
 
 def _cpu_worker_init():
     # one BLAS thread per worker process: the pool provides the parallelism
-    # (numpy is already imported in the parent, so the env var alone is too late)
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     from threadpoolctl import threadpool_limits
 
     threadpool_limits(1)
 
 
-def run_cpu(series, spec, wl_kw, restarts, sample, cores, full_epochs=1000):
-    from concurrent.futures import ProcessPoolExecutor
+def cpu_jobs(series, spec, wl_kw, full_epochs=1000):
+    """Every (series, kind) task of restart 0 (run seed 0), longest first."""
+    kinds = wl_kw.get("kinds", ("pnn", "brbpnn"))
+    bh = wl_kw.get("br_hidden", 1)
+    jobs = []
+    for s in series:
+        for kind in kinds:
+            h = (bh(s.key) if callable(bh) else bh) if kind == "brbpnn" else 1
+            cost = len(s) * (300.0 if kind == "pnn" else 20.0 * h * h)
+            jobs.append((cost, (s.key, s.X, s.y, kind, spec.mode.value, spec.fraction, 0, h, full_epochs)))
+    jobs.sort(key=lambda j: -j[0])
+    return [j for _, j in jobs]
 
-    jobs = cpu_sample_tasks(series, spec, wl_kw, restarts, sample, full_epochs)
+
+def run_cpu(series, spec, wl_kw, cores, full_epochs=1000, sample=None):
+    """The reference algorithm (oracle port) on the host: every task of
+    restart 0 through a process pool of ``cores`` workers (the best CPU mode;
+    wall clock), the serial rate from the same per-task seconds, and the
+    reference's own GIL-thread fan-out (``run_experiment(workers=cores)``,
+    experiment.py:397-401) on a stratified 48-task subset."""
+    from concurrent.futures import ProcessPoolExecutor, ThreadPoolExecutor
+
+    jobs = cpu_jobs(series, spec, wl_kw, full_epochs)
+    if sample:
+        jobs = jobs[::max(1, len(jobs) // sample)][:sample]
     t0 = time.perf_counter()
     with ProcessPoolExecutor(max_workers=cores, initializer=_cpu_worker_init) as pool:
-        secs = list(pool.map(_cpu_task, jobs, chunksize=1))
+        res = list(pool.map(_cpu_task, jobs, chunksize=1))
     wall = time.perf_counter() - t0
-    # ideal-pool throughput: every core busy, mean per-model time of the
-    # stratified sample (favourable to the CPU: ignores the straggler tail)
-    wide = any(j[3] == "brbpnn" and j[7] >= CPU_WIDE_HIDDEN for j in jobs)
-    return {"models_per_s": cores * len(jobs) / sum(secs), "wall_s": wall, "n": len(jobs),
-            "mean_model_s": sum(secs) / len(jobs),
-            "note": (f"; BR-BPNN h>={CPU_WIDE_HIDDEN} fits timed for {CPU_EPOCH_SAMPLE} epochs and "
-                     f"scaled to {full_epochs:.0f} epochs" if wide else "")}
+    secs = [r[0] for r in res]
+    sampled = any(r[1] for r in res)
+    n = len(jobs)
+    sub = jobs[::max(1, n // 48)][:min(48, n)]
+    _cpu_worker_init()
+    t1 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=cores) as tp:
+        tres = list(tp.map(_cpu_task, sub))
+    twall = time.perf_counter() - t1
+    out = {
+        "n": n, "wall_s": wall, "cpu_s": sum(secs),
+        # sampled wide fits have no real wall clock: ideal pool over the scaled seconds
+        "pool_models_per_s": (cores * n / sum(secs)) if sampled else n / wall,
+        "ideal_pool_models_per_s": cores * n / sum(secs),
+        "serial_models_per_s": n / sum(secs),
+        "threads_models_per_s": len(sub) / (twall if not any(r[1] for r in tres) else sum(r[0] for r in tres)),
+        "threads_tasks": len(sub),
+        "cpu_model": cpu_model(), "cores": cores, "sampled": sampled, "subset": bool(sample),
+    }
+    return out
+
+
+def cpu_sample_text(r, workload):
+    s = (f"{'all ' if not r.get('subset') else 'a stratified subset of '}{r['n']} tasks of "
+         f"{workload} restart 0 (run seed 0), oracle/bbml_oracle.py "
+         f"(bit-identical to the reference), process pool of {r['cores']} workers "
+         f"(1 BLAS thread each), longest first: wall {r['wall_s']:.1f} s, {r['cpu_s']:.1f} CPU-s; "
+         f"serial {r['serial_models_per_s']:.2f} models/s (sum of per-task seconds); "
+         f"reference GIL-thread mode (workers={r['cores']}) {r['threads_models_per_s']:.2f} models/s "
+         f"on {r['threads_tasks']} stratified tasks; CPU {r['cpu_model']}")
+    if r["sampled"]:
+        s += (f"; BR-BPNN h>={CPU_WIDE_HIDDEN} fits timed for {CPU_EPOCH_SAMPLE} epochs and scaled "
+              "to the device's epochs (value = ideal pool over the scaled seconds)")
+    return s
 
 
 def reference_arm(args, world, rank):
@@ -228,33 +280,82 @@ def reference_arm(args, world, rank):
     series, spec, kw = workload_series(args.workload)
     restarts = args.restarts or DEFAULT_RESTARTS[args.workload]
     cores = os.cpu_count() or 1
-    sample = args.cpu_sample or max(32, 4 * cores)
-    vals = []
-    for i in range(args.warmup + args.steps):
-        r = run_cpu(series, spec, kw, restarts, sample, cores)
-        if i >= args.warmup:
-            vals.append(r)
-    v = float(np.mean([r["models_per_s"] for r in vals]))
+    r = run_cpu(series, spec, kw, cores, sample=args.cpu_sample)
+    v = r["pool_models_per_s"]
     line = {
         "metric": "models trained/sec", "value": v, "unit": "models/s", "impl": "reference",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * float(np.mean([r["wall_s"] for r in vals])),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": args.workload, "restarts": restarts},
+        "n_gpus": args.gpus, "steps": 1, "warmup": 0, "ms_per_step": 1e3 * r["wall_s"],
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": args.workload, "restarts_per_gpu": restarts, "split": spec.mode.value,
+                   "sample": "restart 0 (the other restarts are the same shapes under other seeds)",
+                   "steps_note": "one pass over every task of restart 0 is the CPU arm's step; "
+                                 f"--steps {args.steps} --warmup {args.warmup} are not repeated "
+                                 "so the arm ends within minutes"},
         "cpu_baseline": {"value": v, "unit": "models/s", "cores": cores, "kind": "port",
-                         "sample": f"{vals[0]['n']} stratified tasks/step (one median pick per "
-                                   f"equal-count cost stratum) of the {args.workload} workload; "
-                                   "ideal-pool throughput = cores / mean per-model seconds; "
-                                   "oracle/bbml_oracle.py (bit-identical to the reference)"
-                                   + vals[0]["note"]},
+                         "sample": cpu_sample_text(r, args.workload),
+                         "serial": r["serial_models_per_s"], "threads": r["threads_models_per_s"],
+                         "ideal_pool": r["ideal_pool_models_per_s"], "cpu_model": r["cpu_model"]},
         "e2e": {"value": v, "unit": "models/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    out = json.dumps(line)
+    print(out, flush=True)
+    if args.json_out:
+        with open(args.json_out, "w") as fh:
+            fh.write(out + "\n")
 
 
 # ---------------------------------------------------------------------------
 # GPU side
 # ---------------------------------------------------------------------------
+
+def shard_units(series, spec, kw, restarts, world, rank):
+    """Strong scaling: the fixed (series, restart) unit list, LPT-sharded by
+    cost (sharding.lpt_assign); returns (units of this rank, all shards)."""
+    from paper_2202_07798_b200 import sharding
+
+    bh = kw.get("br_hidden", 1)
+    kinds = kw.get("kinds", ("pnn", "brbpnn"))
+    frac = spec.fraction if spec.mode.value == "random" else 0.5
+    units, costs = [], []
+    for r in range(restarts):
+        for i, s in enumerate(series):
+            h = bh(s.key) if callable(bh) else bh
+            c = sum(sharding.task_cost(len(s) * frac, k, d=s.arity, h=h) for k in kinds)
+            units.append((i, r))
+            costs.append(c)
+    shards = sharding.lpt_assign(costs, world)
+    units = np.array(units, dtype=np.int64)
+    return units[shards[rank]], [units[s] for s in shards]
+
+
+class Gather:
+    """Strong-scaling result gather (the one collective): every rank's
+    per-model status (raw bytes), metrics (4 doubles) and weights, padded to
+    the largest shard, all-gathered over NCCL into rank-ordered buffers."""
+
+    def __init__(self, torch, dist, dev, world):
+        self.torch, self.dist, self.dev, self.world = torch, dist, dev, world
+        sizes = torch.tensor([dev.status.numel(), dev.metrics.numel(), dev.weights.numel()],
+                             dtype=torch.int64, device="cuda")
+        allsz = [torch.zeros_like(sizes) for _ in range(world)]
+        dist.all_gather(allsz, sizes)
+        self.max = torch.stack(allsz).max(0).values.tolist()
+        self.bufs = [torch.zeros(m, dtype=t, device="cuda") for m, t in
+                     zip(self.max, (torch.uint8, torch.float64, torch.float64))]
+        self.out = [torch.zeros(world * m, dtype=t, device="cuda") for m, t in
+                    zip(self.max, (torch.uint8, torch.float64, torch.float64))]
+
+    def __call__(self):
+        for src, buf, out in zip((self.dev.status, self.dev.metrics, self.dev.weights), self.bufs, self.out):
+            buf[:src.numel()].copy_(src)
+            self.dist.all_gather_into_tensor(out, buf)
+        return 3
+
+    @property
+    def bytes(self) -> int:
+        return sum(b.numel() * b.element_size() for b in self.out)
+
 
 def main():
     args = parse()
@@ -267,7 +368,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2202_07798_b200 import batch
+    from paper_2202_07798_b200 import batch, prep
     from paper_2202_07798_b200._lib import STATUS
 
     torch.cuda.set_device(local)
@@ -276,15 +377,30 @@ def main():
 
     series, spec, kw = workload_series(args.workload)
     restarts = args.restarts or DEFAULT_RESTARTS[args.workload]
-    my_restarts = list(range(rank * restarts, (rank + 1) * restarts))
-    wl = batch.build_workload(series, spec, restarts=my_restarts, precision=args.precision, **kw)
+    if args.scaling == "strong":
+        units, shards = shard_units(series, spec, kw, restarts, world, rank)
+        build_kw = dict(units=units)
+        total_models_all = sum(len(s) for s in shards) * len(kw.get("kinds", ("pnn", "brbpnn")))
+    else:
+        build_kw = dict(restarts=list(range(rank * restarts, (rank + 1) * restarts)))
+        total_models_all = None
+
+    def build():
+        # the public e2e path starts from the raw series rows
+        return batch.build_workload(series, spec, precision=args.precision,
+                                    table=prep.SeriesTable.from_series(series), **build_kw, **kw)
+
+    wl = build()
     dev = batch.DeviceWorkload(wl)
+    gather = Gather(torch, dist, dev, world) if (world > 1 and args.scaling == "strong") else None
     torch.cuda.synchronize()
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     s = torch.cuda.current_stream()
     for _ in range(args.warmup):
         dev.step()
+        if gather:
+            gather()
     torch.cuda.synchronize()
     st = dev.fetch()["status"]
     n_bad = int((st["code"] != 0).sum())
@@ -295,8 +411,7 @@ def main():
     time.sleep(0.3 if clk else 0)
 
     # device-timed region: K steps, L2 flushed between steps (outside the events)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     launches = 0
     if world > 1:
@@ -304,32 +419,41 @@ def main():
     torch.cuda.synchronize()
     for k in range(args.steps):
         flush.fill_(float(k))
-        a, b, c, d_ = ev[k]
+        a, b = ev[k]
         a.record(s)
-        launches += dev.step_timed(b, c) if hasattr(dev, "step_timed") else dev.step()
-        d_.record(s)
+        launches += dev.step()
+        if gather:
+            gather()
+        b.record(s)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
+    step_ms = [e[0].elapsed_time(e[1]) for e in ev]
     total_s = sum(step_ms) / 1e3
 
-    # clock sampling covers the device-timed region; stopped before the e2e loop
-    # (an nvidia-smi query holds the driver and stalls host-side CUDA calls)
+    # clock sampling covers the device-timed region; stopped before the e2e
+    # loop (an nvidia-smi query holds the driver and stalls host CUDA calls)
     if clk:
         clk.terminate()
         clk.wait()
 
-    # end-to-end: public batched call with pinned host inputs, H2D + D2H every step
-    e2e_times = []
+    # end-to-end: raw series -> batched prep -> pinned -> H2D -> step -> D2H
+    e2e_times, prep_times = [], []
     for k in range(args.steps):
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        batch.fit_predict(wl, dev, predictions=False)  # result: weights, status, metrics
+        wl_k = build()
+        t1 = time.perf_counter()
+        dev.refresh(wl_k)
+        dev.step()
+        if gather:
+            gather()
+        dev.fetch(predictions=False)  # weights, status, per-model metrics
         e2e_times.append(time.perf_counter() - t0)
+        prep_times.append(t1 - t0)
 
-    # dominant kernel (PNN train) timed alone on its stream for the roofline
-    # each training kernel timed alone on its launching stream (CUDA events)
     from paper_2202_07798_b200._lib import check, lib, ptr
 
     def timed(fn):
@@ -344,6 +468,7 @@ def main():
             reps.append(e0.elapsed_time(e1))
         return float(np.mean(reps))
 
+    # each training call timed alone on its launching stream (CUDA events)
     pnn_ms = lm_ms = None
     if len(wl.pnn):
         pnn_ms = timed(lambda: check(lib().bbml_pnn_train(
@@ -363,7 +488,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_s, e2e_step = float(t[0]), float(t[1])  # e2e: mean step, max over ranks
-    models_per_step = wl.n_models * world
+    models_per_step = total_models_all if total_models_all is not None else wl.n_models * world
     value = models_per_step * args.steps / total_s
     e2e_value = models_per_step / e2e_step
 
@@ -372,12 +497,13 @@ def main():
         pnn_fl = sum(pnn_flops(int(r["n"]), int(r["d"]), int(r["h"]), int(r["epochs"]), int(r["batch"]))
                      for r in wl.pnn)
         st_lm = st_all[len(wl.pnn):]
-        lm_fl = sum(lm_flops(int(r["n"]), int(r["d"]), int(r["h"]), int(e), int(t))
-                    for r, e, t in zip(wl.lm, st_lm["epochs"], st_lm["trials"]))
+        lm_fl = sum(lm_flops(int(r["n"]), int(r["d"]), int(r["h"]), int(e), int(tr))
+                    for r, e, tr in zip(wl.lm, st_lm["epochs"], st_lm["trials"]))
         rl = {}
         if pnn_ms:
             a = pnn_fl / (pnn_ms * 1e-3) / 1e12
-            rl["pnn"] = {"bound": f"fp{args.precision}-pipe", "kernel": "pnn_lat_kernel (bbml_pnn_train)",
+            kname = "pnn_f64_kernel" if args.precision == 64 else "pnn_lat_kernel"
+            rl["pnn"] = {"bound": f"fp{args.precision}-pipe", "kernel": f"{kname} (bbml_pnn_train)",
                          "achieved": a, "peak": peak_p, "unit": "TFLOP/s", "frac": a / peak_p,
                          "kernel_ms": pnn_ms, "algorithmic_flops": pnn_fl, "traffic": None}
         if lm_ms:
@@ -388,16 +514,16 @@ def main():
             rl["lm"] = {"bound": "fp64-pipe", "kernel": f"{kn} (bbml_lm_train)",
                         "achieved": a, "peak": peak64, "unit": "TFLOP/s", "frac": a / peak64,
                         "kernel_ms": lm_ms, "algorithmic_flops": lm_fl, "traffic": None}
-        try:  # DRAM bytes per launch of the dominant kernel from the committed ncu capture
-            with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+        try:  # DRAM bytes per launch of each kernel from the committed ncu captures
+            with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as fh:
                 traffic = json.load(fh)
         except (OSError, ValueError):
             traffic = {}
-        for v in rl.values():
-            name = v["kernel"].split(" ")[0]
-            if name in traffic:
-                v["traffic"] = traffic[name]["bytes_per_launch"]
-                v["traffic_source"] = f'{traffic[name]["report"]} ({traffic[name]["launch"]})'
+        for kk, v in rl.items():
+            tr = traffic.get(f"{kk}_fp{args.precision}" if kk == "pnn" else kk)
+            if tr and tr.get("workload") == args.workload:
+                v["traffic"] = tr["bytes_per_launch"]
+                v["traffic_source"] = tr["report"]
         dom = max(rl, key=lambda k: rl[k]["kernel_ms"]) if rl else None
         roof = dict(rl[dom]) if dom else {}
         roof["peak_source"] = ("measured: bbml_fma_peak FMA-pipe microbenchmark on this GPU "
@@ -408,28 +534,33 @@ def main():
             cores = os.cpu_count() or 1
             wide_ep = (float(st_lm["epochs"][wl.lm["h"] >= CPU_WIDE_HIDDEN].mean())
                        if len(wl.lm) and (wl.lm["h"] >= CPU_WIDE_HIDDEN).any() else 1000.0)
-            r = run_cpu(series, spec, kw, restarts, args.cpu_sample or max(32, 4 * cores), cores,
-                        wide_ep)
-            cpu = {"value": r["models_per_s"], "unit": "models/s", "cores": cores, "kind": "port",
-                   "sample": f"{r['n']} stratified tasks (median pick per equal-count cost stratum) "
-                             f"of {args.workload}; ideal-pool throughput = cores / mean per-model "
-                             f"seconds ({r['mean_model_s']:.3f} s); wall {r['wall_s']:.1f} s"
-                             + r["note"]}
+            r = run_cpu(series, spec, kw, cores, wide_ep, sample=args.cpu_sample)
+            cpu = {"value": r["pool_models_per_s"], "unit": "models/s", "cores": cores, "kind": "port",
+                   "sample": cpu_sample_text(r, args.workload), "serial": r["serial_models_per_s"],
+                   "threads": r["threads_models_per_s"], "ideal_pool": r["ideal_pool_models_per_s"],
+                   "cpu_model": r["cpu_model"]}
+        tb = dev.table_bytes
         line = {
             "metric": "models trained/sec", "value": value, "unit": "models/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32" if args.precision == 32 else "f64",
+            "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None,
+            "dtype": "f32" if args.precision == 32 else "f64",
             "data": "synthetic",
-            "config": {"workload": args.workload, "restarts_per_gpu": restarts,
-                       "models_per_gpu": wl.n_models, "pnn_models": len(wl.pnn),
-                       "br_models": len(wl.lm), "pnn_precision": f"fp{args.precision}",
-                       "br_precision": "fp64", "l2": "flushed (256 MiB write) between steps",
-                       "split": spec.mode.value},
-            "e2e": {"value": e2e_value, "unit": "models/s", "h2d_bytes_per_step": dev.h2d_bytes,
+            "config": {"workload": args.workload,
+                       ("restarts_per_gpu" if args.scaling == "weak" else "restarts_total"): restarts,
+                       "models_per_gpu": wl.n_models, "models_per_step": models_per_step,
+                       "pnn_models": len(wl.pnn), "br_models": len(wl.lm),
+                       "pnn_precision": f"fp{args.precision}", "br_precision": "fp64",
+                       "l2": "flushed (256 MiB write) between steps", "split": spec.mode.value},
+            "e2e": {"value": e2e_value, "unit": "models/s",
+                    "h2d_bytes_per_step": dev.h2d_bytes + tb,
                     "d2h_bytes_per_step": dev.d2h_bytes_for(False),
+                    "prep_ms_per_step": 1e3 * float(np.mean(prep_times)),
                     "result": "trained weights + status + per-model test MSE / Pearson / "
-                              "Spearman (bbml_metrics)"},
+                              "Spearman (bbml_metrics); inputs re-split / normalised / packed "
+                              "from the raw series rows every step (prep.py)"
+                              + ("; + NCCL all-gather of every shard's results" if gather else "")},
             "roofline": roof,
             "gpu_launches": launches,
             "models_failed": n_bad,
@@ -441,8 +572,10 @@ def main():
             "clocks": summarize_clocks(clock_path, local),
             "cpu_baseline": cpu,
             "step_ms": step_ms,
-            "e2e_step_ms": [1e3 * t for t in e2e_times],
+            "e2e_step_ms": [1e3 * x for x in e2e_times],
         }
+        if gather:
+            line["e2e"]["gather_bytes_per_step"] = gather.bytes
         out = json.dumps(line)
         print(out, flush=True)
         if args.json_out:

@@ -85,11 +85,15 @@ class Workload:
 def build_workload(series: Sequence[BbSeries], spec: SplitSpec, *, kinds=("pnn", "brbpnn"),
                    restarts: Sequence[int] = (0,), pnn_epochs=300, pnn_batch=10, pnn_lr=1e-4,
                    pnn_hidden=10, br_hidden: int | Callable = 1, br_max_epochs=1000,
-                   precision=64, table: Optional[prep.SeriesTable] = None) -> Workload:
+                   precision=64, table: Optional[prep.SeriesTable] = None,
+                   units: Optional[np.ndarray] = None) -> Workload:
     """Split + normalise every series once (``prep.prepare``: whole-array
     passes with the reference's traces.py semantics), then one PNN and/or BR
     task per (series, restart); restart r seeds the model with
-    experiment.series_seed(r, key, kind)."""
+    experiment.series_seed(r, key, kind).  ``units``
+    ((U, 2) int array of (series index, restart)) replaces the full
+    series x restarts product with an explicit list (a strong-scaling shard);
+    units whose series failed to split are dropped."""
     t = prep.SeriesTable.from_series(series) if table is None else table
     P = prep.prepare(t, spec.mode.value, spec.fraction, spec.seed)
     keys = list(t.keys)
@@ -112,14 +116,26 @@ def build_workload(series: Sequence[BbSeries], spec: SplitSpec, *, kinds=("pnn",
         if kind not in kinds or not len(ok):
             tabs[kind] = (None, np.zeros(0, np.int64), np.zeros(0, np.int64))
             continue
+        kc = zlib.crc32(kind.encode())
+        if units is None:
+            pairs = [(ok, int(r)) for r in restarts]
+        else:
+            u = np.asarray(units, dtype=np.int64).reshape(-1, 2)
+            u = u[ok_mask[u[:, 0]]]
+            pairs = [(u[u[:, 1] == r, 0], int(r)) for r in np.unique(u[:, 1])]
+            order = np.concatenate([np.flatnonzero(u[:, 1] == r) for r in np.unique(u[:, 1])]) \
+                if len(u) else np.zeros(0, np.int64)
         seeds, sidx = [], []
-        for r in restarts:
-            seeds.append(engine.series_seed_table(int(r), app_crc[ok], kid[ok], bid[ok],
-                                                  np.full(len(ok), zlib.crc32(kind.encode()),
-                                                          dtype=np.uint64)))
-            sidx.append(ok)
-        seeds = np.concatenate(seeds)
-        sidx = np.concatenate(sidx)
+        for si, r in pairs:
+            seeds.append(engine.series_seed_table(r, app_crc[si], kid[si], bid[si],
+                                                  np.full(len(si), kc, dtype=np.uint64)))
+            sidx.append(si)
+        seeds = np.concatenate(seeds) if seeds else np.zeros(0, dtype=_lib.SEED)
+        sidx = np.concatenate(sidx) if sidx else np.zeros(0, np.int64)
+        if units is not None and len(sidx):  # back to the caller's unit order
+            inv = np.empty_like(order)
+            inv[order] = np.arange(len(order))
+            seeds, sidx = seeds[inv], sidx[inv]
         rb, n, d = train.row_begin[sidx], train.n[sidx], d_ser[sidx]
         if kind == "pnn":
             tab, Pn = engine.pnn_tasks(rb, n, d, pnn_hidden, pnn_epochs, pnn_batch, pnn_lr, 1e-8,
@@ -196,6 +212,31 @@ class DeviceWorkload:
     def upload(self):
         for _, dst, src in self._inputs():
             dst.copy_(src, non_blocking=True)
+
+    def refresh(self, wl: Workload) -> None:
+        """Load a freshly prepared workload of the same shapes (e.g. the same
+        series re-split and re-normalised from raw rows): host arrays into
+        the pinned staging buffers, task tables replaced, then H2D."""
+        torch = self.torch
+        torch.cuda.current_stream(self.device).synchronize()  # staging may still feed the last H2D
+        new = {"X": wl.train.X, "y": wl.train.y, "Xq": wl.test.X, "yq": wl.test.y,
+               "yq_raw": wl.test_raw_y, "norms": wl.norm_rows().ravel()}
+        for name, _, dst in self._inputs():
+            a = np.ascontiguousarray(new[name], dtype=np.float64)
+            if a.size != dst.numel():
+                raise ValueError(f"refresh: {name} has {a.size} values, the resident workload {dst.numel()}")
+            dst.numpy().reshape(a.shape)[...] = a
+        if len(wl.pnn) != self.n_p or len(wl.lm) != self.n_l:
+            raise ValueError("refresh: model count changed")
+        self.wl = wl
+        self.pnn_tab = np.ascontiguousarray(wl.pnn)
+        self.lm_tab = np.ascontiguousarray(wl.lm)
+        self.upload()
+
+    @property
+    def table_bytes(self) -> int:
+        """Task tables the library uploads per step (train, predict, metrics)."""
+        return (self.pnn_tab.nbytes + self.lm_tab.nbytes + self.pred_tab.nbytes + self.met_tab.nbytes)
 
     @property
     def h2d_bytes(self) -> int:

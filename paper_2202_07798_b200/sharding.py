@@ -79,11 +79,15 @@ def train_many_distributed(pairs: Sequence[tuple], config, *, group=None, **kw) 
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    hidden_of = kw.get("br_hidden_of")
     costs = []
-    for series, kind in pairs:
-        n = len(series) * (config.fraction if config.split_mode.value == "random" else 0.5)
+    for pair in pairs:  # (series, kind) or (series, kind, SplitSpec) as train_many takes
+        series, kind = pair[0], pair[1]
+        sp = pair[2] if len(pair) > 2 else config.split_spec()
+        n = len(series) * (sp.fraction if sp.mode.value == "random" else 0.5)
+        h = hidden_of(series) if hidden_of is not None else config.br_hidden
         costs.append(task_cost(n, kind, epochs=config.pnn_epochs, batch=config.pnn_batch_size,
-                               d=series.arity, h=config.br_hidden, max_epochs=config.br_max_epochs))
+                               d=series.arity, h=h, max_epochs=config.br_max_epochs))
     shards = lpt_assign(costs, world)
     mine = shards[rank]
     local = experiment.train_many([pairs[i] for i in mine], config, **kw).results if mine else []

@@ -75,3 +75,60 @@ def test_gather_ordered_world_size_2_gloo():
         assert [g[0] for g in got] == list(range(len(costs)))  # original order
         assert all(g[1] == owner[g[0]] for g in got)           # produced by its owner
     assert out[0] == out[1]
+
+
+def _dist_worker(rank, world, port, q):
+    """Runs sharding.train_many_distributed's real shard -> train -> gather
+    path with experiment.train_many replaced by a CPU mock (no GPU here)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2202_07798_b200 import experiment, synth
+        from paper_2202_07798_b200.experiment import BatchOutput, ExperimentConfig, SeriesResult
+        from paper_2202_07798_b200.traces import BbSeries, SplitMode, SplitSpec
+
+        seen = []
+
+        def mock_train_many(pairs, config, **kw):
+            seen.extend((p[0].key, p[1], p[2].fraction if len(p) > 2 else None) for p in pairs)
+            hid = kw.get("br_hidden_of")
+            return BatchOutput([SeriesResult(p[0].key, p[1], n_train=hid(p[0]) if hid else -1,
+                                             mse=float(rank)) for p in pairs])
+
+        experiment.train_many = mock_train_many
+        series = [BbSeries(k, X, y) for k, X, y in synth.app20()[:7]]
+        specs = [SplitSpec(SplitMode.RANDOM, f, 1) for f in (0.3, 0.7)]
+        pairs = [(s, k, sp) for s in series for k in ("pnn", "brbpnn") for sp in specs]
+        cfg = ExperimentConfig(split_mode=SplitMode.RANDOM)
+        out = sharding.train_many_distributed(pairs, cfg, br_hidden_of=lambda s: 3 + s.key[2])
+        q.put((rank, [(r.key, r.kind, r.n_train, r.mse) for r in out], seen,
+               [(p[0].key, p[1], p[2].fraction) for p in pairs]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_train_many_distributed_world_size_2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(2):
+        rank, res, seen, pairs = q.get(timeout=180)
+        out[rank] = (res, seen, pairs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res0, seen0, pairs = out[0]
+    res1, seen1, _ = out[1]
+    assert res0 == res1                                   # every rank holds the full, ordered result
+    assert [(r[0], r[1]) for r in res0] == [(p[0], p[1]) for p in pairs]
+    assert sorted(seen0 + seen1) == sorted(pairs)         # each task trained exactly once
+    assert seen0 and seen1                                # both ranks got work
+    owner = {t: 0 for t in seen0} | {t: 1 for t in seen1}
+    for r, p in zip(res0, pairs):
+        assert r[3] == float(owner[p])                    # result produced by the owning rank
+        assert r[2] == 3 + p[0][2]                        # br_hidden_of reached the local call
