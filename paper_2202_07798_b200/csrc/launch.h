@@ -46,6 +46,7 @@ struct LmLaunch {
   double* weights;
   double* history;
   bbml_model_status* status;
+  int* queue;  // persistent warp kernels: next-task counter (nullptr: static grid)
 };
 
 // The library's stream-ordered memory pool for the current device: the

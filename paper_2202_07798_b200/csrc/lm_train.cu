@@ -19,6 +19,7 @@
 // (the reference recomputes the identical J at the same w each trial).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -1002,12 +1003,10 @@ constexpr int lm_min_blocks() {
 // over the warps and reduced in warp order through shared memory; the
 // damped solve and the eigen-solve run on warp 0; the scalar LM / evidence
 // bookkeeping is computed identically by every warp.
-template <int PM, int D, int NW = 1>
-__global__ void __launch_bounds__(NW > 1 ? 32 * NW : (PM > 8 ? 32 * LM32_WARPS : 128),
-                                  NW > 1 ? 1 : lm_min_blocks<PM, D>()) lm_warp_kernel(LmLaunch L) {
-  extern __shared__ __align__(16) unsigned char lm_smem[];
-  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  const int64_t task = NW > 1 ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * (blockDim.x >> 5) + wi;
+// One BR-BPNN fit (brbpnn.train) by one warp (NW = 1) or one CTA of NW warps.
+template <int PM, int D, int NW>
+__device__ __forceinline__ void lm_fit_task(const LmLaunch& L, int64_t task, unsigned char* lm_smem,
+                                            int lane, int wi) {
   if (task >= L.n_tasks) return;
   WarpLm<PM>& S = NW > 1 ? *(WarpLm<PM>*)lm_smem : ((WarpLm<PM>*)lm_smem)[wi];
   // NW > 1: cross-warp partials + broadcast slots after the model workspace
@@ -1260,6 +1259,42 @@ __global__ void __launch_bounds__(NW > 1 ? 32 * NW : (PM > 8 ? 32 * LM32_WARPS :
   }
 }
 
+// NW > 1: one model per CTA (blockIdx.x).  NW = 1 with L.queue set: a
+// persistent grid of warps, each pulling the next model index from an
+// atomic counter over the cost-sorted task list, so a warp whose fit
+// early-stopped (BR fits stop anywhere between ~10 and 1000 epochs) takes
+// the next model instead of idling until its CTA's slowest fit ends
+// (SURVEY §8e).  Without a queue: one model per warp, static.
+template <int PM, int D, int NW = 1>
+__global__ void __launch_bounds__(NW > 1 ? 32 * NW : (PM > 8 ? 32 * LM32_WARPS : 128),
+                                  NW > 1 ? 1 : lm_min_blocks<PM, D>()) lm_warp_kernel(LmLaunch L) {
+  extern __shared__ __align__(16) unsigned char lm_smem[];
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  if constexpr (NW > 1) {
+    lm_fit_task<PM, D, NW>(L, (int64_t)blockIdx.x, lm_smem, lane, wi);
+  } else if (L.queue == nullptr) {
+    lm_fit_task<PM, D, 1>(L, (int64_t)blockIdx.x * (blockDim.x >> 5) + wi, lm_smem, lane, wi);
+  } else {
+    while (true) {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(L.queue, 1);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= L.n_tasks) break;
+      lm_fit_task<PM, D, 1>(L, t, lm_smem, lane, wi);
+      __syncwarp();
+    }
+  }
+}
+
+// persistent warps by default (BBML_LM_QUEUE=0: static one-model-per-warp grid)
+static bool lm_queue_on() {
+  static const bool on = [] {
+    const char* e = getenv("BBML_LM_QUEUE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int PM, int D>
 static cudaError_t lm_launch_warp(const LmLaunch& L, cudaStream_t s) {
   const int warps = PM > 8 ? LM32_WARPS : 4;
@@ -1269,7 +1304,15 @@ static cudaError_t lm_launch_warp(const LmLaunch& L, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  k<<<(int)ceil_div(L.n_tasks, warps), 32 * warps, smem, s>>>(L);
+  int blocks = (int)ceil_div(L.n_tasks, warps);
+  if (L.queue != nullptr) {  // one resident wave of persistent warps
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * warps, smem);
+    blocks = std::min(blocks, std::max(1, per_sm) * sms);
+  }
+  k<<<blocks, 32 * warps, smem, s>>>(L);
   return cudaGetLastError();
 }
 
@@ -1363,6 +1406,10 @@ bbml_status lm_train_launch(const bbml_lm_task* tasks, int32_t n_tasks, const do
                                x_stride, weights, history, status, scratch, stream, true,
                                &wide_slabs)) != BBML_OK)
         return st;
+  int* queues = nullptr;  // one work counter per shape group (persistent warp kernels)
+  if ((st = scratch.alloc(&queues, (int64_t)groups.size())) != BBML_OK) return st;
+  if (cudaMemsetAsync(queues, 0, groups.size() * sizeof(int), stream) != cudaSuccess)
+    return cuda_status(cudaGetLastError(), "lm queue reset");
   StreamFork fork(stream, (int)groups.size());  // shape groups run concurrently
   for (size_t gno = 0; gno < groups.size(); ++gno) {
     const int begin = groups[gno].first, end = groups[gno].second;
@@ -1386,6 +1433,9 @@ bbml_status lm_train_launch(const bbml_lm_task* tasks, int32_t n_tasks, const do
     L.weights = weights;
     L.history = history;
     L.status = status;
+    if (b < 100 && lm_queue_on()) {  // per-group work counter, zeroed on the group's stream
+      L.queue = queues + gno;
+    }
     cudaError_t e;
     if (b == 101) e = lm_launch_multi<1>(L, cs);
     else if (b == 102) e = lm_launch_multi<2>(L, cs);

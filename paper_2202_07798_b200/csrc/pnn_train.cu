@@ -1261,6 +1261,11 @@ template <int DM, int SP, typename PermT>
 __global__ void __launch_bounds__(256, 1) pnn_f64_kernel(PnnLaunch L) {
   pnn_f64_body<DM, SP, PermT>(L);
 }
+// long series, 128 registers: two CTAs (or one plus shorter work) per SM
+template <int DM, int SP, typename PermT>
+__global__ void __launch_bounds__(256, 2) pnn_f64_kernel_half(PnnLaunch L) {
+  pnn_f64_body<DM, SP, PermT>(L);
+}
 // short series: 4 consumer + 1 shared producer warp
 template <int DM, int SP, typename PermT>
 __global__ void __launch_bounds__(160, 3) pnn_f64_kernel_shared(PnnLaunch L) {
@@ -1284,6 +1289,18 @@ static int env_int(const char* name, int dflt) {
 }
 static int f64_long_npw() {
   static const int v = env_int("BBML_F64_LONG_NPW", 4);
+  return v;
+}
+static int f64_long_groups() {
+  static const int v = env_int("BBML_F64_LONG_GROUPS", 4);
+  return (v == 1 || v == 2) ? v : 4;
+}
+static int f64_long_minb() {
+  static const int v = env_int("BBML_F64_LONG_MINB", 1);
+  return v;
+}
+static int f64_short_npw() {
+  static const int v = env_int("BBML_F64_SHORT_NPW", 1);
   return v;
 }
 static int f64_short_minb() {
@@ -1362,9 +1379,13 @@ static cudaError_t launch_variant(PnnLaunch L, int64_t nmax, size_t smem_limit, 
   // model (one sequential Fisher-Yates scan keeps up with one consumer warp).
   // Short series (n < kLongSeries): one producer serves the 4 models, so the
   // CTA is 5 warps and eight CTAs fit per SM.
-  const bool shared_prod = LAT && nmax < kLongSeries;
-  const int groups_max = 4;
-  const int npw_long = !LAT ? groups_max : sizeof(T) == 8 ? f64_long_npw() : long_npw();
+  const bool shared_prod = LAT && nmax < kLongSeries && !(sizeof(T) == 8 && f64_short_npw() > 1);
+  // FP64 long series: models per CTA (BBML_F64_LONG_GROUPS; fewer models per
+  // CTA = a smaller register footprint, so other groups co-reside on the SM)
+  const int groups_max = (sizeof(T) == 8 && LAT && !shared_prod) ? f64_long_groups() : 4;
+  const int npw_long = !LAT ? groups_max
+                     : sizeof(T) == 8 ? (nmax < kLongSeries ? f64_short_npw() : f64_long_npw())
+                                      : long_npw();
   const int npw_max = shared_prod ? 1 : npw_long;
   const size_t flags = pnn_smem_header(groups_max, groups_max);
   const size_t per_group = 2 * (size_t)nmax * sizeof(PermT);
@@ -1393,10 +1414,11 @@ static cudaError_t launch_variant(PnnLaunch L, int64_t nmax, size_t smem_limit, 
     smem = L.stage_off + (size_t)groups * f64_stage_doubles<DM, 5>() * sizeof(double);
   }
   auto k = !LAT ? pnn_train_kernel<T, DM, HM, G, SC, PermT>
-                : F64 ? (npw == 1 ? (f64_short_minb() == 4 ? pnn_f64_kernel_shared4<DM, 5, PermT>
-                                                           : pnn_f64_kernel_shared<DM, 5, PermT>)
-                         : npw == 2 ? pnn_f64_kernel_np2<DM, 5, PermT>
-                                    : pnn_f64_kernel<DM, 5, PermT>)
+                : F64 ? (shared_prod ? (f64_short_minb() == 4 ? pnn_f64_kernel_shared4<DM, 5, PermT>
+                                                              : pnn_f64_kernel_shared<DM, 5, PermT>)
+                         : npw < groups ? pnn_f64_kernel_np2<DM, 5, PermT>
+                         : f64_long_minb() == 2 ? pnn_f64_kernel_half<DM, 5, PermT>
+                                                : pnn_f64_kernel<DM, 5, PermT>)
                       : (npw == 1 ? pnn_lat_kernel_shared<T, DM, 5, PermT>
                                   : npw == 2 ? pnn_lat_kernel_np2<T, DM, 5, PermT>
                                              : pnn_lat_kernel<T, DM, 5, PermT>);
@@ -1486,6 +1508,9 @@ bbml_status pnn_train_launch(const bbml_pnn_task* tasks, int32_t n_tasks, const 
     if (ka != kb) return ka < kb;
     return cost(a) > cost(b);
   });
+  auto cost_sorted = [](const bbml_pnn_task& t) {
+    return (double)t.epochs * (double)((t.n + t.batch - 1) / t.batch);
+  };
   std::vector<bbml_pnn_task> sorted(n_tasks);
   std::vector<int32_t> orig(n_tasks);
   std::vector<int64_t> poff(n_tasks);
@@ -1550,6 +1575,19 @@ bbml_status pnn_train_launch(const bbml_pnn_task* tasks, int32_t n_tasks, const 
     }
     groups_rng.push_back({b0, b1});
     b0 = b1;
+  }
+  // the group holding the longest sequential chain launches first, so its
+  // CTAs are resident before the shorter groups fill the SMs
+  // (off by default: A/B on suite16 FP64, tools/r2k.sh -- the long CTAs then
+  // hold whole SMs while the BR-BPNN call waits; step 1089 -> 1126 ms)
+  if (env_int("BBML_PNN_LONG_FIRST", 0)) {
+    auto chain = [&](const std::pair<int, int>& g) {
+      double c = 0.0;
+      for (int i = g.first; i < g.second; ++i) c = std::max(c, cost_sorted(sorted[i]));
+      return c;
+    };
+    std::stable_sort(groups_rng.begin(), groups_rng.end(),
+                     [&](const std::pair<int, int>& a, const std::pair<int, int>& b) { return chain(a) > chain(b); });
   }
   StreamFork fork(stream, (int)groups_rng.size());
   for (size_t gno = 0; gno < groups_rng.size(); ++gno) {

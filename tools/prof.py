@@ -16,6 +16,7 @@ ap.add_argument("--epochs", type=int, default=300)
 ap.add_argument("--only-long", action="store_true")
 ap.add_argument("--top", type=int, default=0)
 ap.add_argument("--app", default=None)
+ap.add_argument("--not-app", default=None)
 ap.add_argument("--br-epochs", type=int, default=1000)
 ap.add_argument("--reps", type=int, default=3)
 a = ap.parse_args()
@@ -23,7 +24,11 @@ series, spec, kw = bench.workload_series(a.workload)
 if a.only_long:
     series = sorted(series, key=lambda s: -len(s))[:1]
 if a.app:
-    series = [s for s in series if s.key[0] == a.app]
+    apps = set(a.app.split(","))
+    series = [s for s in series if s.key[0] in apps]
+if a.not_app:
+    apps = set(a.not_app.split(","))
+    series = [s for s in series if s.key[0] not in apps]
 if a.top:
     series = sorted(series, key=lambda s: -len(s))[:a.top]
 kinds = {"both": ("pnn", "brbpnn"), "pnn": ("pnn",), "br": ("brbpnn",)}[a.kind]
