@@ -11,6 +11,8 @@
  *                                                     solve_damped 153-171, evidence_update 221-251)
  *   bbml_predict      <- bbcount/pnn.py:108-118      pnn.forward
  *   bbml_metrics      <- bbcount/metrics.py:33-76    mse / pearson / spearman
+ *   bbml_pooled_metrics <- bbcount/experiment.py:180-206 pooled per-app correlations
+ *   bbml_heatmaps     <- bbcount/metrics.py:145-156  heatmap_data (experiment.py:331-338)
  *                        bbcount/brbpnn.py:85-91     brbpnn.forward
  *                        bbcount/persist.py:35-43    SavedModel.predict_normalized / predict_counts
  *   bbml_pnn_loss_grad<- bbcount/pnn.py:121-147      pnn.loss_and_grads (unit level)
@@ -152,11 +154,26 @@ bbml_status bbml_predict(const bbml_pred_task* tasks, int32_t n_tasks, const dou
    series' [x_min(d), x_max(d), y_min, y_max] in norm.  Writes 4 doubles at
    out_offset: mse (normalised space), pearson and spearman of the de-normalised
    predictions vs actual_raw (NaN = undefined: constant vector or n < 2), and
-   1.0 if Spearman / Pearson were computed on the device (0.0 when n > 4096:
-   the caller computes them). */
+   1.0 (Pearson / Spearman computed: always, any n -- test sets over 4096 rows
+   take a counting-rank path in global memory). */
 bbml_status bbml_metrics(const bbml_pred_task* tasks, int32_t n_tasks, const double* pred,
                          const double* actual_norm, const double* actual_raw,
                          const double* norm, double* out, void* stream);
+/* Pooled correlations per group of models (experiment.summarize, experiment.py:
+   180-206: Pearson / Spearman of the concatenated de-normalised predictions vs
+   raw counts of every successful model of an (app, kind)).  seg_of: HOST, the
+   group of each task (tasks of a group concatenate in task order).  out
+   (device): 2 doubles per group {pearson, spearman}, NaN when undefined. */
+bbml_status bbml_pooled_metrics(const bbml_pred_task* tasks, int32_t n_tasks,
+                                const int32_t* seg_of, int32_t n_seg, const double* pred,
+                                const double* actual_raw, const double* norm, double* out,
+                                void* stream);
+/* Per-model prediction-vs-actual heatmaps (metrics.heatmap_data, metrics.py:145-156):
+   edges (device, bins+1 doubles per task) = linspace(0, max(pred, actual) or 1, bins+1),
+   counts (device, bins*bins int32 per task, [pred_bin][actual_bin]) of histogram2d. */
+bbml_status bbml_heatmaps(const bbml_pred_task* tasks, int32_t n_tasks, const double* pred,
+                          const double* actual_raw, const double* norm, int32_t bins,
+                          double* edges, int32_t* counts, void* stream);
 
 /* ---- unit-level kernels (one model per task; rows at row_begin, n rows) ---- */
 /* loss[i] and grads (P doubles at w_offset of grads) of the batch NLL */

@@ -290,3 +290,55 @@ def metrics(pred, actual_norm, actual_raw, pred_offset, row_begin, n, d, norms, 
     check(lib().bbml_metrics(ptr(t), M, ptr(pd), ptr(an), ptr(ar), ptr(nd), ptr(out),
                              _stream(torch)), "bbml_metrics")
     return out.cpu().numpy()[:4 * M].reshape(M, 4)
+
+
+def _met_tasks(pred_offset, row_begin, n, d, norm_rows_count, width):
+    M = len(n)
+    t = np.zeros(M, dtype=PRED_TASK)
+    t["row_begin"] = row_begin
+    t["n"] = n
+    t["w_offset"] = pred_offset
+    t["d"] = d
+    t["h"] = 1
+    t["norm_offset"] = np.arange(M, dtype=np.int64) * width
+    return t
+
+
+def pooled_metrics(groups, pred, actual_raw, pred_offset, row_begin, n, d, norms, device=None):
+    """Pooled Pearson / Spearman per group of models on the device
+    (``bbml_pooled_metrics``; experiment.summarize, experiment.py:180-206):
+    model i (in ``groups[i]``) contributes its de-normalised predictions and
+    raw counts; groups concatenate in model order.  Returns (G, 2) host
+    float64, NaN = undefined."""
+    torch = torch_cuda()
+    dev = torch.device("cuda" if device is None else device)
+    groups = np.ascontiguousarray(groups, dtype=np.int32)
+    G = int(groups.max()) + 1 if len(groups) else 0
+    if G == 0:
+        return np.zeros((0, 2))
+    norms = np.ascontiguousarray(norms, dtype=np.float64)
+    t = _met_tasks(pred_offset, row_begin, n, d, len(n), norms.shape[1])
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)  # noqa: E731
+    pd, ar, nd = up(pred), up(actual_raw), up(norms.ravel())
+    out = torch.empty(2 * G, dtype=torch.float64, device=dev)
+    check(lib().bbml_pooled_metrics(ptr(t), len(t), ptr(groups), G, ptr(pd), ptr(ar), ptr(nd),
+                                    ptr(out), _stream(torch)), "bbml_pooled_metrics")
+    return out.cpu().numpy().reshape(G, 2)
+
+
+def heatmaps(pred, actual_raw, pred_offset, row_begin, n, d, norms, bins, device=None):
+    """Per-model heatmap edges (M, bins+1) and counts (M, bins, bins) on the
+    device (``bbml_heatmaps``; metrics.heatmap_data)."""
+    torch = torch_cuda()
+    dev = torch.device("cuda" if device is None else device)
+    norms = np.ascontiguousarray(norms, dtype=np.float64)
+    t = _met_tasks(pred_offset, row_begin, n, d, len(n), norms.shape[1])
+    M = len(t)
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)  # noqa: E731
+    pd, ar, nd = up(pred), up(actual_raw), up(norms.ravel())
+    edges = torch.empty(max(M, 1) * (bins + 1), dtype=torch.float64, device=dev)
+    counts = torch.empty(max(M, 1) * bins * bins, dtype=torch.int32, device=dev)
+    check(lib().bbml_heatmaps(ptr(t), M, ptr(pd), ptr(ar), ptr(nd), int(bins), ptr(edges), ptr(counts),
+                              _stream(torch)), "bbml_heatmaps")
+    return (edges.cpu().numpy()[:M * (bins + 1)].reshape(M, bins + 1),
+            counts.cpu().numpy()[:M * bins * bins].reshape(M, bins, bins))

@@ -273,7 +273,14 @@ def train_many(pairs: Sequence[tuple], config: ExperimentConfig, *, precision: O
         W = np.concatenate([fetched[k][0].w(j) for k, j, _ in all_tasks])
         woff = engine.offsets(engine.n_params(dd, hh))
         pred_flat = engine.predict(W, woff, dd, hh, kk, q, None, eps=pnn.DEFAULT_EPS)
-        launches += 1
+        # per-model test metrics on the device (bbml_metrics): MSE in the
+        # normalised space, Pearson / Spearman of the de-normalised predictions
+        yq = np.concatenate([t.prep.yte for _, _, t in all_tasks])
+        yq_raw = np.concatenate([t.prep.yte_raw for _, _, t in all_tasks])
+        Dq = max(1, int(dd.max()))
+        norm_rows = np.stack([t.prep.norm.row(Dq) for _, _, t in all_tasks])
+        met = engine.metrics(pred_flat, yq, yq_raw, q.row_begin, q.row_begin, q.n, dd, norm_rows)
+        launches += 2
     for a, (kind, j, t) in enumerate(all_tasks):
         i = order[kind][j]
         res = results[i]
@@ -291,12 +298,12 @@ def train_many(pairs: Sequence[tuple], config: ExperimentConfig, *, precision: O
         d = t.prep.Xtr.shape[1]
         w = rk.w(j)
         pred = pred_flat[int(q.row_begin[a]):int(q.row_begin[a]) + int(q.n[a])]
-        res.mse = metrics.mse(pred, t.prep.yte)
+        res.mse = float(met[a, 0])
         res.pred_raw = t.prep.norm.inverse_targets(pred)
         res.actual_raw = t.prep.yte_raw
         if len(pred) >= 2:
-            res.pearson = metrics.pearson(res.pred_raw, res.actual_raw)
-            res.spearman = metrics.spearman(res.pred_raw, res.actual_raw)
+            res.pearson = None if math.isnan(met[a, 1]) else float(met[a, 1])
+            res.spearman = None if math.isnan(met[a, 2]) else float(met[a, 2])
         seed = _lib.seedseq_u64(list(_seed_entropy(seed_rec)))
         if kind == "pnn":
             model = pnn.PnnModel.from_packed(w, d, t.hidden)
@@ -342,20 +349,39 @@ class AppSummary:
 
 
 def summarize(rows: Sequence[SeriesResult], split_mode: SplitMode) -> list:
-    """Per (app, kind) pooled summary (experiment.py:180-206)."""
+    """Per (app, kind) summary (experiment.py:180-206): mean test MSE of the
+    successful fits and the pooled Pearson / Spearman of all their
+    de-normalised predictions vs raw counts -- every group's correlations in
+    one device call (bbml_pooled_metrics, counting ranks)."""
     groups: dict = {}
     for r in rows:
         groups.setdefault((r.key[0], r.kind), []).append(r)
+    keys = sorted(groups)
+    seg, preds, acts = [], [], []
+    for g, k in enumerate(keys):
+        for r in groups[k]:
+            if r.error is None:
+                seg.append(g)
+                preds.append(np.asarray(r.pred_raw, dtype=float))
+                acts.append(np.asarray(r.actual_raw, dtype=float))
+    pooled = np.full((len(keys), 2), np.nan)
+    if seg:
+        n = np.array([len(p) for p in preds], dtype=np.int32)
+        off = engine.offsets(n.astype(np.int64))
+        ident = np.tile([0.0, 1.0, 0.0, 1.0], (len(n), 1))  # predictions already de-normalised
+        res = engine.pooled_metrics(np.array(seg, np.int32), np.concatenate(preds), np.concatenate(acts),
+                                    off, off, n, np.ones(len(n), np.int32), ident)
+        pooled[:len(res)] = res
     out = []
-    for (app, kind), grp in sorted(groups.items()):
+    for g, (app, kind) in enumerate(keys):
+        grp = groups[(app, kind)]
         ok = [r for r in grp if r.error is None]
         avg = float(np.mean([r.mse for r in ok])) if ok else None
-        preds = np.concatenate([r.pred_raw for r in ok]) if ok else np.array([])
-        acts = np.concatenate([r.actual_raw for r in ok]) if ok else np.array([])
+        total = sum(len(r.pred_raw) for r in ok)
+        pear = None if total < 2 or math.isnan(pooled[g, 0]) else float(pooled[g, 0])
+        spear = None if total < 2 or math.isnan(pooled[g, 1]) else float(pooled[g, 1])
         out.append(AppSummary(app, kind, len(grp), len(grp) - len(ok), avg,
-                              None if avg is None else metrics.accuracy_percent(avg),
-                              metrics.pearson(preds, acts) if preds.size >= 2 else None,
-                              metrics.spearman(preds, acts) if preds.size >= 2 else None,
+                              None if avg is None else metrics.accuracy_percent(avg), pear, spear,
                               any(r.constant_target for r in ok), any(r.pinned_hyperparams for r in ok)))
     return out
 
@@ -483,20 +509,100 @@ def write_curve_csv(points: Sequence[CurvePoint], path: Path) -> None:
 
 
 def write_split_manifests(series_list: Sequence[BbSeries], spec: SplitSpec, out_dir: Path) -> None:
+    """splits_<app>.csv: every trace row with its partition (experiment.py:
+    344-362); the labels of all series come from one batched prep pass."""
+    table = prep.SeriesTable.from_series(series_list)
+    labels, errors = prep.split_labels(table, spec.mode.value, spec.fraction, spec.seed)
+    names = np.array(["discarded", "train", "test"], dtype=object)
     by_app: dict = {}
-    for s in series_list:
-        by_app.setdefault(s.key[0], []).append(s)
-    for app, grp in sorted(by_app.items()):
+    for i, s in enumerate(series_list):
+        by_app.setdefault(s.key[0], []).append(i)
+    for app, idx in sorted(by_app.items()):
+        lines = [",".join(trace_header(series_list[idx[0]].arity) + ["partition"])]
+        for i in idx:
+            s = series_list[i]
+            a, b = int(table.offsets[i]), int(table.offsets[i + 1])
+            # a constant-feature range split labels the whole series "error"
+            bad = i in errors and "are constant" in errors[i]
+            lab = ["error"] * (b - a) if bad else names[labels[a:b]]
+            head = f"{s.key[0]},{s.key[1]},{s.key[2]},"
+            for row, count, l in zip(s.X, s.y, lab):
+                lines.append(head + ",".join(str(int(v)) for v in row) + f",{int(count)},{l}")
         with open(out_dir / f"splits_{app}.csv", "w", encoding="utf-8", newline="\n") as fh:
-            fh.write(",".join(trace_header(grp[0].arity) + ["partition"]) + "\n")
-            for s in grp:
-                try:
-                    labels = classify(s, spec)
-                except SplitError:
-                    labels = np.full(len(s), "error", dtype=object)
-                for row, count, lab in zip(s.X, s.y, labels):
-                    params = ",".join(str(int(v)) for v in row)
-                    fh.write(f"{s.key[0]},{s.key[1]},{s.key[2]},{params},{int(count)},{lab}\n")
+            fh.write("\n".join(lines) + "\n")
+
+
+def device_heatmaps(rows: Sequence[SeriesResult], bins: int):
+    """Heatmap edges / counts of every successful row in one device call
+    (bbml_heatmaps); returns (row indices, edges (M, bins+1), counts (M, bins, bins))."""
+    idx = [i for i, r in enumerate(rows)
+           if r.error is None and r.pred_raw is not None and len(r.pred_raw)]
+    if not idx:
+        return idx, np.zeros((0, bins + 1)), np.zeros((0, bins, bins), np.int32)
+    preds = [np.asarray(rows[i].pred_raw, dtype=float) for i in idx]
+    n = np.array([len(p) for p in preds], dtype=np.int32)
+    off = engine.offsets(n.astype(np.int64))
+    ident = np.tile([0.0, 1.0, 0.0, 1.0], (len(idx), 1))  # predictions already de-normalised
+    edges, counts = engine.heatmaps(np.concatenate(preds),
+                                    np.concatenate([np.asarray(rows[i].actual_raw, float) for i in idx]),
+                                    off, off, n, np.ones(len(idx), np.int32), ident, bins)
+    return idx, edges, counts
+
+
+def write_models_columnar(rows: Sequence[SeriesResult], path: Path) -> int:
+    """Every saved model of a run in ONE columnar file (numpy .npz): keys,
+    kinds, shapes, seeds, flat pack-order weights + offsets, normalisers,
+    BR hyperparameters and per-model config JSON.  ``export_models_json``
+    turns it into the reference's per-model JSON (schema v1) files."""
+    saved = [r.saved for r in rows if r.saved is not None]
+    M = len(saved)
+    d = np.array([m.model.n_inputs for m in saved], dtype=np.int32)
+    h = np.array([m.model.hidden for m in saved], dtype=np.int32)
+    w = [np.concatenate([np.ravel(m.model.W1), m.model.b1, m.model.W2, [m.model.b2]]) for m in saved]
+    D = max(1, int(d.max())) if M else 1
+    np.savez(path,
+             app=np.array([m.key[0] for m in saved], dtype=object).astype(str),
+             kernel_id=np.array([m.key[1] for m in saved], dtype=np.int64),
+             bb_id=np.array([m.key[2] for m in saved], dtype=np.int64),
+             kind=np.array([m.kind for m in saved]).astype(str), d=d, h=h,
+             seed=np.array([str(m.seed) for m in saved]).astype(str),
+             weights=np.concatenate(w) if w else np.zeros(0),
+             w_offset=engine.offsets(np.array([len(x) for x in w], dtype=np.int64)) if M else np.zeros(0, np.int64),
+             norm=np.stack([m.normalizer.row(D) for m in saved]) if M else np.zeros((0, 2 * D + 2)),
+             eps=np.array([getattr(m.model, "eps", np.nan) for m in saved]),
+             alpha=np.array([getattr(m.model, "alpha", np.nan) for m in saved]),
+             beta=np.array([getattr(m.model, "beta", np.nan) for m in saved]),
+             config=np.array([json.dumps(m.config) for m in saved]).astype(str))
+    return M
+
+
+def read_models_columnar(path: Union[str, Path]) -> list:
+    """SavedModel objects back from ``models.npz``."""
+    z = np.load(path, allow_pickle=False)
+    out = []
+    for i in range(len(z["d"])):
+        d, h = int(z["d"][i]), int(z["h"][i])
+        w = z["weights"][int(z["w_offset"][i]):int(z["w_offset"][i]) + h * (d + 2) + 1]
+        hd = h * d
+        W1, b1, W2, b2 = w[:hd].reshape(h, d).copy(), w[hd:hd + h].copy(), w[hd + h:hd + 2 * h].copy(), float(w[-1])
+        kind = str(z["kind"][i])
+        model = (pnn.PnnModel(W1, b1, W2, b2, eps=float(z["eps"][i])) if kind == "pnn" else
+                 brbpnn.BrbpnnModel(W1, b1, W2, b2, alpha=float(z["alpha"][i]), beta=float(z["beta"][i])))
+        row = z["norm"][i]
+        norm = Normalizer(row[:d].copy(), row[d:2 * d].copy(), float(row[2 * d]), float(row[2 * d + 1]))
+        key = (str(z["app"][i]), int(z["kernel_id"][i]), int(z["bb_id"][i]))
+        out.append(SavedModel(kind, model, norm, key, int(z["seed"][i]), json.loads(str(z["config"][i]))))
+    return out
+
+
+def export_models_json(columnar: Union[str, Path], out_dir: Union[str, Path]) -> int:
+    """The reference layout (models/<slug>.json, schema v1) from models.npz."""
+    out_dir = Path(out_dir)
+    out_dir.mkdir(parents=True, exist_ok=True)
+    models = read_models_columnar(columnar)
+    for m in models:
+        save_model(m, out_dir / f"{series_slug(m.key, m.kind)}.json")
+    return len(models)
 
 
 def digest_file(path: Union[str, Path]) -> str:
@@ -516,9 +622,20 @@ class ExperimentOutput:
 
 def run_experiment(series_list: Sequence[BbSeries], config: ExperimentConfig,
                    out_dir: Union[str, Path], input_digests: Optional[dict] = None,
-                   br_hidden_of=None) -> ExperimentOutput:
+                   br_hidden_of=None, layout: str = "files") -> ExperimentOutput:
     """experiment.py:385-451 with ONE batched device call for all tasks
-    (``workers`` is accepted for compatibility; results never depend on it)."""
+    (``workers`` is accepted for compatibility; results never depend on it).
+
+    ``layout="files"`` writes the reference's artifact tree (report.csv,
+    summary.csv, splits_<app>.csv, models/<slug>.json, heatmap_<slug>.csv,
+    kde_<slug>.csv, manifest.json).  ``layout="columnar"`` keeps report /
+    summary / splits / manifest and replaces the per-model files with
+    models.npz, heatmaps.npz and kde.npz (one file each however many models:
+    cfg 4 has 320k of them); ``export_models_json`` recovers the JSON files.
+    Heatmaps and the summary correlations come from the device in one call
+    each."""
+    if layout not in ("files", "columnar"):
+        raise ValueError(f"layout must be 'files' or 'columnar', got {layout!r}")
     started = time.time()
     out_dir = Path(out_dir)
     out_dir.mkdir(parents=True, exist_ok=True)
@@ -531,20 +648,34 @@ def run_experiment(series_list: Sequence[BbSeries], config: ExperimentConfig,
     write_report_csv(rows, out_dir / "report.csv")
     write_summary_csv(summaries, config.split_mode, out_dir / "summary.csv")
     write_split_manifests(series_list, config.split_spec(), out_dir)
-    models_dir = out_dir / "models"
-    models_dir.mkdir(exist_ok=True)
-    for r in rows:
-        if r.saved is not None:
-            save_model(r.saved, models_dir / f"{series_slug(r.key, r.kind)}.json")
-        if r.error is None and r.pred_raw is not None and r.pred_raw.size:
-            write_heatmap_csv(metrics.heatmap_data(r.pred_raw, r.actual_raw, config.heatmap_bins),
-                              out_dir / f"heatmap_{series_slug(r.key, r.kind)}.csv")
+    hm_idx, hm_edges, hm_counts = device_heatmaps(rows, config.heatmap_bins)
+    kdes = []
     for s in series_list:
         try:
-            curve = metrics.kde(s.y)
+            kdes.append((s.key, metrics.kde(s.y)))
         except (metrics.BandwidthError, metrics.MetricShapeError):
             continue
-        write_kde_csv(curve, out_dir / f"kde_{series_slug(s.key)}.csv")
+    if layout == "files":
+        models_dir = out_dir / "models"
+        models_dir.mkdir(exist_ok=True)
+        for r in rows:
+            if r.saved is not None:
+                save_model(r.saved, models_dir / f"{series_slug(r.key, r.kind)}.json")
+        for j, i in enumerate(hm_idx):
+            r = rows[i]
+            write_heatmap_csv(metrics.HeatmapData(hm_edges[j], hm_counts[j]),
+                              out_dir / f"heatmap_{series_slug(r.key, r.kind)}.csv")
+        for key, curve in kdes:
+            write_kde_csv(curve, out_dir / f"kde_{series_slug(key)}.csv")
+    else:
+        write_models_columnar(rows, out_dir / "models.npz")
+        np.savez(out_dir / "heatmaps.npz",
+                 slug=np.array([series_slug(rows[i].key, rows[i].kind) for i in hm_idx]).astype(str),
+                 edges=hm_edges, counts=hm_counts)
+        np.savez(out_dir / "kde.npz", slug=np.array([series_slug(k) for k, _ in kdes]).astype(str),
+                 grid=np.stack([c.grid for _, c in kdes]) if kdes else np.zeros((0, 256)),
+                 density=np.stack([c.density for _, c in kdes]) if kdes else np.zeros((0, 256)),
+                 bandwidth=np.array([c.bandwidth for _, c in kdes]))
     manifest = {
         "config": config.to_manifest(),
         "inputs": input_digests or {},

@@ -256,6 +256,42 @@ def gen_train_one():
     save("train_one", d)
 
 
+def gen_experiment():
+    """The reference's run_experiment artifacts (acceptance criterion 8's
+    configuration -- linear family, grid n=1:60, high-low, both models, 60
+    PNN / 100 BR epochs, seed 17 -- plus three more apps so the summary has
+    several groups): summary.csv, report.csv, one model JSON / heatmap / kde
+    file per kind, the splits manifest."""
+    import tempfile
+    from pathlib import Path
+
+    from bbcount.experiment import run_experiment
+
+    series = _family("linear", (tuple(range(1, 61)),))
+    series += [(k, X, y) for k, X, y in synth.app20()[:4]]
+    series += _family("trilinear", (tuple(range(12, 19, 2)),) * 3)[:2]
+    ref_series = [_ref_series(k, X, y) for k, X, y in series]
+    cfg = ExperimentConfig(split_mode=SplitMode.HIGH_LOW, fraction=0.7, seed=17, pnn_epochs=60,
+                           br_max_epochs=100)
+    d = {"n_series": np.array(len(series))}
+    for i, (k, X, y) in enumerate(series):
+        d[f"s{i}_key"] = np.array([k[0], str(k[1]), str(k[2])])
+        d[f"s{i}_X"], d[f"s{i}_y"] = np.asarray(X, float), np.asarray(y, float)
+    with tempfile.TemporaryDirectory() as tmp:
+        run_experiment(ref_series, cfg, tmp)
+        out = Path(tmp)
+        files = ["summary.csv", "report.csv"]
+        files += sorted(p.name for p in out.glob("splits_*.csv"))[:2]
+        files += sorted(p.name for p in out.glob("heatmap_*.csv"))[:3]
+        files += sorted(p.name for p in out.glob("kde_*.csv"))[:2]
+        files += ["models/" + p.name for p in sorted((out / "models").glob("*.json"))[:4]]
+        d["files"] = np.array(files)
+        for j, f in enumerate(files):
+            d[f"f{j}"] = np.array((out / f).read_text())
+        d["all_files"] = np.array(sorted(str(p.relative_to(out)) for p in out.rglob("*") if p.is_file()))
+    save("experiment", d)
+
+
 def gen_pnn_long():
     """Long-series PNN case (the bench's longest sequential chain): the first
     suite16 pathfinder series, random split 0.7 / seed 0 and the reference's
@@ -282,6 +318,10 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["pnn_long"]:
         gen_pnn_long()
         sys.exit(0)
+    if sys.argv[1:] == ["experiment"]:
+        gen_experiment()
+        sys.exit(0)
+    gen_experiment()
     gen_pnn_long()
     gen_rng()
     gen_pnn()

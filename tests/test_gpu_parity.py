@@ -301,6 +301,21 @@ def test_train_one_matches_reference_golden(golden):
             assert abs(r.mse - float(g[p + "mse"])) <= tol * max(1.0, abs(float(g[p + "mse"]))), (key, kind)
             got = r.saved.predict_counts(g[p + "raw_q"])
             assert _rel(got, g[p + "counts_q"], floor) <= tol, (key, kind)
+            # device Pearson / Spearman (experiment.py:150-152): Pearson against
+            # the reference's value; Spearman against the oracle on the device's
+            # own predictions (saturated fits predict exactly tied values, so
+            # 1e-16 prediction differences move ranks by 1/2) and against the
+            # reference's value when its predictions have no ties
+            pw, sw = (float(v) for v in g[p + "corr"])
+            assert (r.pearson is None) == np.isnan(pw), (key, kind, r.pearson, pw)
+            if r.pearson is not None:
+                assert abs(r.pearson - pw) <= 1e-6, (key, kind, r.pearson, pw)
+            so = O.spearman(r.pred_raw, r.actual_raw)
+            assert (r.spearman is None) == (so is None), (key, kind, r.spearman, so)
+            if so is not None:
+                assert abs(r.spearman - so) <= 1e-12, (key, kind, r.spearman, so)
+                if len(np.unique(g[p + "pred_raw"])) == len(g[p + "pred_raw"]):
+                    assert abs(r.spearman - sw) <= 1e-6, (key, kind, r.spearman, sw)
             checked += 1
     assert checked >= 60
 
@@ -419,16 +434,19 @@ def test_br_hidden1_long_series_multiwarp():
         assert e <= max(1e-3, 25 * spread), (k, e, spread)
 
 
-def test_device_metrics_match_metrics_py():
-    """bbml_metrics against metrics.py: MSE in the normalised
-    space, Pearson / Spearman (average-rank ties) of de-normalised predictions
-    vs raw counts, undefined -> NaN / None; random and tie-heavy vectors,
-    constant vectors, n = 1, and a > 4096-row set left to the host."""
-    from paper_2202_07798_b200 import engine, metrics
+def test_device_metrics_match_oracle():
+    """bbml_metrics / bbml_pooled_metrics / bbml_heatmaps
+    against the oracle's restatement of metrics.py (bit-identical to the
+    reference, tests/test_oracle_golden.py): MSE in the normalised space,
+    Pearson / Spearman (tie-averaged ranks) of de-normalised predictions,
+    undefined -> NaN; random and tie-heavy vectors, constants, n = 1, and test
+    sets beyond the shared-memory sort (counting-rank path); pooled groups;
+    heatmap edges bit-identical and counts equal."""
+    from paper_2202_07798_b200 import engine
 
     rng = np.random.default_rng(4)
-    sizes = [1, 2, 3, 7, 50, 333, 1000, 4096, 5000]
-    preds, an, ar, norms, ds = [], [], [], [], []
+    sizes = [1, 2, 3, 7, 50, 333, 1000, 4096, 5000, 9000]
+    preds, an, ar, norms = [], [], [], []
     for k, n in enumerate(sizes):
         p = rng.normal(size=n)
         a = rng.normal(size=n)
@@ -442,23 +460,43 @@ def test_device_metrics_match_metrics_py():
         an.append(a)
         ar.append(np.round(a * (hi - lo) + lo, 3))
         norms.append([0.0, 1.0, lo, hi])
-        ds.append(1)
     off = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
-    out = engine.metrics(np.concatenate(preds), np.concatenate(an), np.concatenate(ar), off, off,
-                         np.array(sizes, np.int32), np.array(ds, np.int32), np.array(norms))
+    nn = np.array(sizes, np.int32)
+    ones = np.ones(len(sizes), np.int32)
+    out = engine.metrics(np.concatenate(preds), np.concatenate(an), np.concatenate(ar), off, off, nn,
+                         ones, np.array(norms))
     for k, n in enumerate(sizes):
         p, a, raw = preds[k], an[k], ar[k]
         lo, hi = norms[k][2], norms[k][3]
-        assert abs(out[k, 0] - metrics.mse(p, a)) <= 1e-12 * max(1.0, metrics.mse(p, a))
+        want_mse = float(np.mean((p - a) ** 2))
+        assert abs(out[k, 0] - want_mse) <= 1e-12 * max(1.0, want_mse)
+        assert out[k, 3] == 1.0
         if n < 2:
-            assert np.isnan(out[k, 1]) and np.isnan(out[k, 2]) and out[k, 3] == 1.0
-            continue
-        if n > 4096:
-            assert out[k, 3] == 0.0
+            assert np.isnan(out[k, 1]) and np.isnan(out[k, 2])
             continue
         pr = p * (hi - lo) + lo
-        for col, ref in ((1, metrics.pearson(pr, raw)), (2, metrics.spearman(pr, raw))):
+        for col, ref in ((1, O.pearson(pr, raw)), (2, O.spearman(pr, raw))):
             if ref is None:
                 assert np.isnan(out[k, col]), (n, col)
             else:
                 assert abs(out[k, col] - ref) <= 1e-12, (n, col, out[k, col], ref)
+    # pooled groups (experiment.summarize): groups 0 = sizes[3:6], 1 = sizes[6:], 2 = sizes[:3]
+    grp = np.array([2, 2, 2, 0, 0, 0, 1, 1, 1, 1], np.int32)
+    pooled = engine.pooled_metrics(grp, np.concatenate(preds), np.concatenate(ar), off, off, nn, ones,
+                                   np.array(norms))
+    for gi in range(3):
+        ks = [k for k in range(len(sizes)) if grp[k] == gi]
+        pr = np.concatenate([preds[k] * (norms[k][3] - norms[k][2]) + norms[k][2] for k in ks])
+        raw = np.concatenate([ar[k] for k in ks])
+        for col, ref in ((0, O.pearson(pr, raw)), (1, O.spearman(pr, raw))):
+            assert (np.isnan(pooled[gi, col]) if ref is None else abs(pooled[gi, col] - ref) <= 1e-12), \
+                (gi, col, pooled[gi, col], ref)
+    # heatmaps of |de-normalised prediction| vs |raw|: edges bit-identical, counts equal
+    P = [np.abs(p) for p in preds]
+    A = [np.abs(r) for r in ar]
+    edges, counts = engine.heatmaps(np.concatenate(P), np.concatenate(A), off, off, nn, ones,
+                                    np.tile([0.0, 1.0, 0.0, 1.0], (len(sizes), 1)), 32)
+    for k in range(len(sizes)):
+        e, c = O.heatmap(P[k], A[k], 32)
+        assert edges[k].tobytes() == e.tobytes(), k
+        np.testing.assert_array_equal(counts[k], c)

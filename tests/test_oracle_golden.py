@@ -125,3 +125,23 @@ def test_pnn_oracle_matches_reference_long_series(golden):
     w, hist = O.pnn_fit(X, y, X.shape[1], 10, int(g["epochs"]), 10, 1e-4, _seed(g["seed"]))
     np.testing.assert_allclose(w, g["w"], rtol=1e-12, atol=0)
     np.testing.assert_allclose(hist, g["hist"], rtol=1e-12, atol=0)
+
+
+def test_oracle_metrics_reproduce_reference_correlations(golden):
+    """Pearson / Spearman of the reference's own test predictions (golden
+    pred_raw) vs the raw test counts give the reference's r*_corr exactly."""
+    g = golden("train_one")
+    checked = 0
+    for i in range(int(g["n_runs"])):
+        p = f"r{i}_"
+        if str(g[p + "error"]) or len(g[p + "pred_raw"]) < 2:
+            continue
+        app, k, b, kind, mode = (str(v) for v in g[p + "key"])
+        seed = int(g[p + "cfg"][0])
+        lab = O.split_labels(g[p + "X"], mode, 0.7, seed)
+        actual = g[p + "y"][lab == 2]
+        for got, want in ((O.pearson(g[p + "pred_raw"], actual), g[p + "corr"][0]),
+                          (O.spearman(g[p + "pred_raw"], actual), g[p + "corr"][1])):
+            assert (got is None and np.isnan(want)) or got == float(want), (app, k, b, kind)
+        checked += 1
+    assert checked >= 60
