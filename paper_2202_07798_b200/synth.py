@@ -151,3 +151,82 @@ def sweep(n_apps: int, seed: int = 0) -> Iterator:
         coef = tuple(int(c) for c in rng.integers(1, 4, size=4))
         out.extend(app20(f"sweep{i:05d}", coef=coef))
     return out
+
+
+# ---------------------------------------------------------------------------
+# The reference's five builtin families (families.py:64-165) as vectorised
+# closed-form counts, and its trace-CSV dataset format (families.py:330-362,
+# traces.py header): SURVEY §8f f4.  The reference interprets each family's
+# CFG program once per grid point (3.3 s for a 343-point trilinear grid); the
+# counts below are the same integers for every grid point at once, and the
+# writer emits the reference's file byte for byte.
+# ---------------------------------------------------------------------------
+
+# name -> (parameter names, blocks of kernel 0)
+FAMILIES = {
+    "linear": (("n",), 4),
+    "bilinear": (("n", "m"), 5),
+    "trilinear": (("n", "m", "kk"), 5),
+    "triangular": (("n",), 5),
+    "branchy": (("n",), 5),
+}
+
+
+def family_counts(name: str, P: np.ndarray) -> np.ndarray:
+    """(points, blocks) int64 execution counts of kernel 0's blocks at the
+    parameter rows ``P`` (points, arity)."""
+    P = np.asarray(P, dtype=np.int64)
+    one = np.ones(len(P), dtype=np.int64)
+    if name == "linear":
+        n = P[:, 0]
+        cols = [one, n + 1, n, one]
+    elif name == "bilinear":
+        n, m = P[:, 0], P[:, 1]
+        cols = [one, n * (m + 1), n * m, n, one]
+    elif name == "trilinear":
+        n, m, k = P[:, 0], P[:, 1], P[:, 2]
+        cols = [one, n * m * (k + 1), n * m * k, n * m, one]
+    elif name == "triangular":
+        n = P[:, 0]
+        cols = [one, n * (n + 3) // 2, n * (n + 1) // 2, n, one]
+    elif name == "branchy":
+        n = P[:, 0]
+        big = n > BRANCHY_THRESHOLD
+        cols = [one, np.where(big, n + 1, 0), np.where(big, n, 0), np.where(big, 0, 1), one]
+    else:
+        raise KeyError(f"unknown family {name!r}")
+    return np.stack(cols, axis=1)
+
+
+def grid_points(axes) -> np.ndarray:
+    """itertools.product order of the per-parameter value tuples (GridSpec)."""
+    return np.array(list(itertools.product(*axes)), dtype=np.int64).reshape(-1, len(axes))
+
+
+def generate_dataset(name: str, axes, out) -> int:
+    """Write the family's trace CSV over the grid (the reference's
+    ``generate_dataset`` format: header app,kernel_id,bb_id,p0..,count, one
+    row per (grid point, block) in grid order, blocks ascending).  ``out``:
+    path or text stream.  Returns the number of rows."""
+    P = grid_points(axes)
+    C = family_counts(name, P)
+    nb = C.shape[1]
+    params = [",".join(map(str, row)) for row in P.tolist()]
+    head = "app,kernel_id,bb_id," + ",".join(f"p{i}" for i in range(P.shape[1])) + ",count\n"
+    lines = [f"{name},0,{b},{params[i]},{C[i, b]}\n" for i in range(len(P)) for b in range(nb)]
+    text = head + "".join(lines)
+    if isinstance(out, (str, bytes)) or hasattr(out, "__fspath__"):
+        with open(out, "w", encoding="utf-8", newline="") as fh:
+            fh.write(text)
+    else:
+        out.write(text)
+    return len(lines)
+
+
+def family_series(name: str, axes):
+    """The series the reference's ingest of that dataset yields: one per
+    block, key (name, 0, b), X = grid points, y = counts (key order)."""
+    P = grid_points(axes)
+    C = family_counts(name, P).astype(float)
+    X = P.astype(float)
+    return [((name, 0, b), X, C[:, b].copy()) for b in range(C.shape[1])]

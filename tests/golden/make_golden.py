@@ -292,6 +292,26 @@ def gen_experiment():
     save("experiment", d)
 
 
+def gen_families():
+    """The reference's generate_dataset (CFG interpreter) on small grids of
+    each builtin family, and on the app20 grid for the four families app20
+    is made of: trace CSV text and the ingested series."""
+    d = {}
+    grids = {"linear": ((1, 2, 3, 7, 60),), "bilinear": ((1, 2, 5), (3, 4)),
+             "trilinear": ((1, 3), (2, 5), (1, 4)), "triangular": ((1, 2, 9, 20),),
+             "branchy": ((1, 7, 8, 9, 10, 33),)}
+    for name, axes in grids.items():
+        buf = io.StringIO()
+        generate_dataset(family_by_name(name).program, GridSpec(axes), buf)
+        d[f"{name}_csv"] = np.array(buf.getvalue())
+    ax = tuple(range(2, 31, 2))
+    for name, axes in (("bilinear", (ax, ax)), ("triangular", (ax,)), ("linear", (ax,)),
+                       ("branchy", (ax,))):
+        for key, X, y in _family(name, axes):
+            d[f"app_{name}_{key[2]}_X"], d[f"app_{name}_{key[2]}_y"] = X, y
+    save("families", d)
+
+
 def gen_pnn_long():
     """Long-series PNN case (the bench's longest sequential chain): the first
     suite16 pathfinder series, random split 0.7 / seed 0 and the reference's
@@ -321,6 +341,10 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["experiment"]:
         gen_experiment()
         sys.exit(0)
+    if sys.argv[1:] == ["families"]:
+        gen_families()
+        sys.exit(0)
+    gen_families()
     gen_experiment()
     gen_pnn_long()
     gen_rng()
