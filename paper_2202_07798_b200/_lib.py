@@ -39,6 +39,9 @@ STATUS = np.dtype([
     ("code", "<i4"), ("epochs", "<i4"), ("detail", "<i4"), ("trials", "<i4"),
     ("value", "<f8"), ("mu", "<f8"), ("gamma", "<f8"), ("alpha", "<f8"), ("beta", "<f8")])
 
+# device envelope (include/bbml.h)
+MAX_INPUTS, PNN_MAX_HIDDEN, LM_MAX_PARAMS = 16, 64, 512
+
 MODEL_OK, MODEL_DIVERGED, MODEL_NONFINITE_GRAD, MODEL_SINGULAR, MODEL_BAD_TASK = range(5)
 BLOCK_NAMES = ("W1", "b1", "W2", "b2")
 

@@ -322,11 +322,16 @@ def _launches_pnn(tab) -> int:
 
 
 def _launches_lm(tab) -> int:
+    """Kernels bbml_lm_train launches: one per shape group (lm_train.cu
+    lm_key: hidden-1 warp path per d, hidden-1 long-series CTA path per d,
+    P <= 8, P <= 32, wide)."""
     if not len(tab):
         return 0
     P = tab["h"] * (tab["d"] + 2) + 1
-    b = np.where(P <= 8, 8, np.where(P <= 32, 32, np.where(P <= 64, 64, 96)))
-    return len(set(b.tolist()))
+    h1 = (tab["h"] == 1) & (tab["d"] <= 4)
+    key = np.where(h1, np.where(tab["n"] >= 2048, 100 + tab["d"], tab["d"]),
+                   np.where(P <= 8, 8, np.where(P <= 32, 32, 512)))
+    return len(set(key.tolist()))
 
 
 class HostBuffers:

@@ -1499,13 +1499,17 @@ __global__ void __launch_bounds__(LM_NT)
   }
 }
 
+// PMAX <= 96: J'J and the LU / Jacobi workspace in shared memory; PMAX = 512
+// (the wide BR-BPNN shapes, hidden 64 at P = 257): both P x P matrices in a
+// global scratch slab per task (gws), the vectors in shared memory.
 template <int PMAX>
 __global__ void lm_unit_kernel(int mode, const int32_t* __restrict__ Ps,
                                const int64_t* __restrict__ pp_off, const int64_t* __restrict__ p_off,
                                const double* __restrict__ jtj, const double* __restrict__ jtr,
                                const double* __restrict__ w, const double* __restrict__ params,
                                double* __restrict__ out_vec, double* __restrict__ out5,
-                               int32_t* __restrict__ info) {
+                               int32_t* __restrict__ info, double* __restrict__ gws) {
+  constexpr bool kGlobal = PMAX > 96;
   const int t = blockIdx.x;
   const int P = Ps[t];
   extern __shared__ double sm[];
@@ -1516,8 +1520,13 @@ __global__ void lm_unit_kernel(int mode, const int32_t* __restrict__ Ps,
   S.delta = q; q += PMAX;
   S.jtr = q; q += PMAX;
   S.rhs = q; q += PMAX;
-  S.jtj = q; q += PMAX * PMAX;
-  S.A = q; q += PMAX * PMAX;
+  if constexpr (kGlobal) {
+    S.jtj = gws + (int64_t)t * 2 * P * P;
+    S.A = S.jtj + (int64_t)P * P;
+  } else {
+    S.jtj = q; q += PMAX * PMAX;
+    S.A = q; q += PMAX * PMAX;
+  }
   S.Jc = nullptr;
   S.rc = q; q += LM_NT;
   S.cs = q; q += 2 * (PMAX + 2);
@@ -1587,8 +1596,8 @@ bbml_status lm_unit_launch(int mode, const int32_t* P, int32_t n_tasks, const in
   if (n_tasks == 0) return BBML_OK;
   int pmax = 0;
   for (int i = 0; i < n_tasks; ++i) {
-    if (P[i] < 1 || P[i] > 96) {
-      set_error("lm unit task %d: P=%d outside 1..96", i, P[i]);
+    if (P[i] < 1 || P[i] > BBML_LM_MAX_PARAMS) {
+      set_error("lm unit task %d: P=%d outside 1..%d", i, P[i], BBML_LM_MAX_PARAMS);
       return BBML_ERR_UNSUPPORTED;
     }
     pmax = std::max(pmax, P[i]);
@@ -1603,12 +1612,20 @@ bbml_status lm_unit_launch(int mode, const int32_t* P, int32_t n_tasks, const in
   if ((st = scratch.upload(dP, P, n_tasks)) != BBML_OK) return st;
   if ((st = scratch.upload(dpp, pp_offset, n_tasks)) != BBML_OK) return st;
   if ((st = scratch.upload(dp, p_offset, n_tasks)) != BBML_OK) return st;
-  const int PM = 96;
-  const size_t smem = (5 * PM + 2 * PM * PM + LM_NT + 2 * (PM + 2) + LM_WARPS + 2 + (PM + 1) / 2 + 1 + 4) *
+  const bool big = pmax > 96;
+  const int PM = big ? BBML_LM_MAX_PARAMS : 96;
+  const size_t mats = big ? 0 : 2 * (size_t)PM * PM;
+  const size_t smem = (5 * PM + mats + LM_NT + 2 * (PM + 2) + LM_WARPS + 2 + (PM + 1) / 2 + 1 + 4) *
                       sizeof(double);
-  auto k = lm_unit_kernel<96>;
+  double* gws = nullptr;
+  if (big) {  // per-task P x P slabs (sized by the largest P) for J'J and the workspace
+    int64_t per = 0;
+    for (int i = 0; i < n_tasks; ++i) per = std::max<int64_t>(per, 2 * (int64_t)P[i] * P[i]);
+    if ((st = scratch.alloc(&gws, per * n_tasks)) != BBML_OK) return st;
+  }
+  auto k = big ? lm_unit_kernel<BBML_LM_MAX_PARAMS> : lm_unit_kernel<96>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k<<<n_tasks, LM_NT, smem, s>>>(mode, dP, dpp, dp, jtj, jtr, w, params, out_vec, out5, info);
+  k<<<n_tasks, LM_NT, smem, s>>>(mode, dP, dpp, dp, jtj, jtr, w, params, out_vec, out5, info, gws);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_status(e, "lm unit launch");
   (void)n_params_per_task;

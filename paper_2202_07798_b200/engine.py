@@ -266,7 +266,7 @@ def metrics(pred, actual_norm, actual_raw, pred_offset, row_begin, n, d, norms, 
     actual_norm / actual_raw[row_begin[i] : +n[i]]; ``norms`` is (M, 2*d_max+2)
     rows of [x_min(d), x_max(d), y_min, y_max].  Arrays may be host arrays or
     device tensors.  Returns (M, 4) host float64: mse, pearson, spearman (NaN =
-    undefined) and a done flag (0: Pearson / Spearman left to the host, n > 4096)."""
+    undefined) and a done flag (1.0: every model, any n)."""
     torch = torch_cuda()
     dev = torch.device("cuda" if device is None else device)
 

@@ -149,6 +149,20 @@ def _config_error(kind: str, config: ExperimentConfig) -> Optional[str]:
     return f"ValueError: unknown model kind {kind!r}"
 
 
+def _envelope_error(kind: str, d: int, h: int) -> Optional[str]:
+    """Shapes the device kernels do not cover (d <= 16; PNN hidden <= 64;
+    BR-BPNN P = h (d + 2) + 1 <= 512) fail this one series instead of the
+    whole batched launch."""
+    if d > _lib.MAX_INPUTS:
+        return f"UnsupportedShape: {d} inputs exceed the device limit {_lib.MAX_INPUTS}"
+    if kind == "pnn" and h > _lib.PNN_MAX_HIDDEN:
+        return f"UnsupportedShape: PNN hidden {h} exceeds the device limit {_lib.PNN_MAX_HIDDEN}"
+    if kind == "brbpnn" and h * (d + 2) + 1 > _lib.LM_MAX_PARAMS:
+        return (f"UnsupportedShape: BR-BPNN with {h * (d + 2) + 1} parameters exceeds the device "
+                f"limit {_lib.LM_MAX_PARAMS}")
+    return None
+
+
 @dataclass
 class BatchOutput:
     results: list
@@ -226,6 +240,10 @@ def train_many(pairs: Sequence[tuple], config: ExperimentConfig, *, precision: O
             continue
         hidden = config.pnn_hidden if kind == "pnn" else (
             br_hidden_of(series) if br_hidden_of else config.br_hidden)
+        err = _envelope_error(kind, series.arity, int(hidden))
+        if err is not None:  # isolated per series, like any other failure
+            res.error = err
+            continue
         tasks[kind].append(Task(p, kind, int(hidden)))
         order[kind].append(i)
 
