@@ -1275,11 +1275,6 @@ template <int DM, int SP, typename PermT>
 __global__ void __launch_bounds__(160, 4) pnn_f64_kernel_shared4(PnnLaunch L) {
   pnn_f64_body<DM, SP, PermT>(L);
 }
-// 4 consumer + 2 producer warps, 3 CTAs per SM
-template <int DM, int SP, typename PermT>
-__global__ void __launch_bounds__(192, 3) pnn_f64_kernel_np2(PnnLaunch L) {
-  pnn_f64_body<DM, SP, PermT>(L);
-}
 // FP64 CTA shapes (development knobs, defaults from one-box A/B):
 //   BBML_F64_LONG_NPW  = 1 | 2 | 4   producer warps per CTA for n >= kLongSeries
 //   BBML_F64_SHORT_MINB = 3 | 4      CTAs per SM for the shared-producer kernel
@@ -1416,7 +1411,6 @@ static cudaError_t launch_variant(PnnLaunch L, int64_t nmax, size_t smem_limit, 
   auto k = !LAT ? pnn_train_kernel<T, DM, HM, G, SC, PermT>
                 : F64 ? (shared_prod ? (f64_short_minb() == 4 ? pnn_f64_kernel_shared4<DM, 5, PermT>
                                                               : pnn_f64_kernel_shared<DM, 5, PermT>)
-                         : npw < groups ? pnn_f64_kernel_np2<DM, 5, PermT>
                          : f64_long_minb() == 2 ? pnn_f64_kernel_half<DM, 5, PermT>
                                                 : pnn_f64_kernel<DM, 5, PermT>)
                       : (npw == 1 ? pnn_lat_kernel_shared<T, DM, 5, PermT>
