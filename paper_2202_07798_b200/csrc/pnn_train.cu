@@ -222,14 +222,34 @@ __device__ void perm_producer_warp(const PnnLaunch& L, int groups, int pw, int n
         __syncwarp();
         int q = 0;
         if (lane == 0) {
-          while (q < 64 && i > 0) {
-            const uint32_t v = ring[q++] & (0xffffffffu >> __clz(i));
-            if ((int)v <= i) {
-              const PermT t = perm[i];
-              perm[i] = perm[v];
-              perm[v] = t;
-              --i;
+          // draws come in groups of 8 (two 16-byte shared loads) and the next
+          // group is loaded before the current one is scanned, so the serial
+          // accept / swap chain does not wait on the draw loads
+          const uint4* r4 = (const uint4*)ring;
+          uint4 c0 = r4[0], c1 = r4[1];
+#pragma unroll 1
+          for (int g = 0; g < 8 && i > 0; ++g) {
+            uint4 n0 = c0, n1 = c1;
+            if (g < 7) {
+              n0 = r4[2 * g + 2];
+              n1 = r4[2 * g + 3];
             }
+            const uint32_t d8[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              if (i > 0) {
+                ++q;
+                const uint32_t v = d8[k] & (0xffffffffu >> __clz(i));
+                if ((int)v <= i) {
+                  const PermT t = perm[i];
+                  perm[i] = perm[v];
+                  perm[v] = t;
+                  --i;
+                }
+              }
+            }
+            c0 = n0;
+            c1 = n1;
           }
         }
         q = __shfl_sync(FULL, q, 0);
