@@ -32,6 +32,77 @@ __global__ void k(int n, int reps, long long* cyc) {
           if ((int)v <= i) --i;
         }
         draws += q;
+      } else if (MODE == 3 || MODE == 4) {  // 8-draw groups loaded ahead
+        int q = 0;
+        const uint4* r4 = (const uint4*)ring;
+        uint4 c0 = r4[0], c1 = r4[1];
+#pragma unroll 1
+        for (int g = 0; g < 8 && i > 0; ++g) {
+          uint4 n0 = c0, n1 = c1;
+          if (g < 7) { n0 = r4[2 * g + 2]; n1 = r4[2 * g + 3]; }
+          const uint32_t d8[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            if (i > 0) {
+              ++q;
+              const uint32_t v = d8[kk] & (0xffffffffu >> __clz(i));
+              if ((int)v <= i) {
+                if (MODE == 3) { uint16_t t = perm[i]; perm[i] = perm[v]; perm[v] = t; }
+                --i;
+              }
+            }
+          }
+          c0 = n0; c1 = n1;
+        }
+        draws += q;
+      } else if (MODE == 5) {  // 8-draw groups, branch-free accept, predicated swap
+        int q = 0;
+        const uint4* r4 = (const uint4*)ring;
+        uint4 c0 = r4[0], c1 = r4[1];
+#pragma unroll 1
+        for (int g = 0; g < 8 && i > 0; ++g) {
+          uint4 n0 = c0, n1 = c1;
+          if (g < 7) { n0 = r4[2 * g + 2]; n1 = r4[2 * g + 3]; }
+          const uint32_t d8[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const bool live = i > 0;
+            q += live;
+            const uint32_t v = d8[kk] & (0xffffffffu >> __clz(i | 1));
+            const bool acc = live && (int)v <= i;
+            const int ii = acc ? i : 0, vv = acc ? (int)v : 0;   // dummy swap of slot 0 with itself
+            const uint16_t a = perm[ii], b = perm[vv];
+            perm[ii] = b; perm[vv] = a;
+            i -= acc;
+          }
+          c0 = n0; c1 = n1;
+        }
+        draws += q;
+      } else if (MODE == 6) {  // mode 5 + incremental mask (no FLO per draw)
+        int q = 0;
+        uint32_t mask = 0xffffffffu >> __clz(i | 1);
+        const uint4* r4 = (const uint4*)ring;
+        uint4 c0 = r4[0], c1 = r4[1];
+#pragma unroll 1
+        for (int g = 0; g < 8 && i > 0; ++g) {
+          uint4 n0 = c0, n1 = c1;
+          if (g < 7) { n0 = r4[2 * g + 2]; n1 = r4[2 * g + 3]; }
+          const uint32_t d8[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const bool live = i > 0;
+            q += live;
+            const uint32_t v = d8[kk] & mask;
+            const bool acc = live && (int)v <= i;
+            const int ii = acc ? i : 0, vv = acc ? (int)v : 0;
+            const uint16_t a = perm[ii], b = perm[vv];
+            perm[ii] = b; perm[vv] = a;
+            i -= acc;
+            mask = ((uint32_t)i <= (mask >> 1)) ? (mask >> 1) : mask;
+          }
+          c0 = n0; c1 = n1;
+        }
+        draws += q;
       } else {  // swap with the top element kept in a register
         int q = 0;
         uint16_t top = perm[i];
@@ -56,11 +127,15 @@ __global__ void k(int n, int reps, long long* cyc) {
 }
 int main() {
   long long* d; cudaMalloc(&d, 16); long long h[2];
-  for (int mode = 0; mode < 3; ++mode) {
+  for (int mode = 0; mode < 7; ++mode) {
     for (int rep = 0; rep < 2; ++rep) {
       if (mode == 0) k<0><<<1, 32>>>(7604, 100000, d);
       if (mode == 1) k<1><<<1, 32>>>(7604, 100000, d);
       if (mode == 2) k<2><<<1, 32>>>(7604, 100000, d);
+      if (mode == 3) k<3><<<1, 32>>>(7604, 100000, d);
+      if (mode == 4) k<4><<<1, 32>>>(7604, 100000, d);
+      if (mode == 5) k<5><<<1, 32>>>(7604, 100000, d);
+      if (mode == 6) k<6><<<1, 32>>>(7604, 100000, d);
       cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
     }
     printf("mode %d: %.1f cycles per element, %.1f per draw\n", mode, (double)h[0] / 7603, (double)h[0] / h[1]);
