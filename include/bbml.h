@@ -12,7 +12,7 @@
  *   bbml_predict      <- bbcount/pnn.py:108-118      pnn.forward
  *   bbml_metrics      <- bbcount/metrics.py:33-76    mse / pearson / spearman
  *   bbml_pooled_metrics <- bbcount/experiment.py:180-206 pooled per-app correlations
- *   bbml_heatmaps     <- bbcount/metrics.py:145-156  heatmap_data (experiment.py:331-338)
+ *   bbml_heatmaps     <- bbcount/metrics.py:145-156  heatmap_data (experiment.py:417-424)
  *                        bbcount/brbpnn.py:85-91     brbpnn.forward
  *                        bbcount/persist.py:35-43    SavedModel.predict_normalized / predict_counts
  *   bbml_pnn_loss_grad<- bbcount/pnn.py:121-147      pnn.loss_and_grads (unit level)
@@ -24,7 +24,7 @@
  *   bbml_tansig       <- bbcount/brbpnn.py:33-38     tansig (unit level)
  *   bbml_seedseq_generate / bbml_pcg64_state
  *                     <- numpy SeedSequence / default_rng as called at
- *                        pnn.py:226, brbpnn.py:559, experiment.py:38-50
+ *                        pnn.py:226, brbpnn.py:309, experiment.py:38-50
  *
  * Conventions
  *  - Task tables are HOST arrays (read during the call, not retained).

@@ -8,7 +8,7 @@ Third-party dependency restated here: NumPy (the reference pins only
 ``numpy>=1.24``, ``pkg/pyproject.toml:10``; fixtures were generated with
 numpy 2.3.5).  The reference draws from it at:
 
-* ``pnn.py:226`` / ``brbpnn.py:559`` — ``np.random.default_rng(seed)``
+* ``pnn.py:226`` / ``brbpnn.py:309`` — ``np.random.default_rng(seed)``
   (SeedSequence -> PCG64 seeding),
 * ``pnn.py:100-103`` / ``brbpnn.py:326-329`` — ``Generator.uniform`` in the
   order W1 (row-major), b1, W2, b2,
@@ -20,7 +20,7 @@ Published algorithms restated (NumPy ``bit_generator.pyx`` SeedSequence,
 ``pcg64.h`` PCG-XSL-RR 128/64, ``distributions.c`` ``random_interval`` with
 masked rejection over the buffered 32-bit stream, ``_shuffle_raw``
 Fisher-Yates from the top index down).  Checked bit-for-bit against
-``numpy.random.default_rng`` in ``tests/test_oracle_rng.py``.
+``numpy.random.default_rng`` in ``tests/test_oracle_golden.py``.
 """
 
 from __future__ import annotations

@@ -1075,7 +1075,7 @@ __device__ __forceinline__ void lm_fit_task(const LmLaunch& L, int64_t task, uns
     }
   };
 
-  if (lead && lane == 0) {  // init (brbpnn.py:323-331)
+  if (lead && lane == 0) {  // init (brbpnn.py:63-82, called at 309-310)
     Pcg64 rng;
     rng.seed(tk.seed);
     const double s1 = __ddiv_rn(1.0, __dsqrt_rn((double)d));

@@ -352,7 +352,7 @@ bbml_status pooled_metrics_launch(const bbml_pred_task* tasks, int32_t n_tasks, 
 
 // ---------------------------------------------------------------------------
 // Per-model heatmaps (metrics.heatmap_data, metrics.py:145-156, written per
-// model by experiment.py:331-338): square bins over [0, max(pred, actual)]
+// model by experiment.py:417-424): square bins over [0, max(pred, actual)]
 // (1.0 when that max is <= 0), edges = numpy.linspace(0, hi, bins + 1)
 // (i * (hi / bins), last edge exactly hi), counts of histogram2d: bin =
 // searchsorted(edges, v, 'right') - 1, a value equal to the last edge goes to
