@@ -51,9 +51,10 @@ struct WideLaunch {
   double* weights;
   double* history;
   bbml_model_status* status;
-  double* scratch;        // per CTA slab
+  double* scratch;        // one slab per resident CTA
   int64_t slab_doubles;   // doubles per slab
   int32_t ld;             // leading dimension of the P x P matrices (>= P, multiple of 4)
+  int* queue;             // next-task counter of the persistent grid
 };
 
 struct WideSmem {
@@ -689,11 +690,10 @@ __device__ double wide_gamma(double* A, const double* jtj, int ld, int P, double
   return g;
 }
 
-__global__ void __launch_bounds__(WNT) lm_wide_kernel(WideLaunch L) {
-  const int task = blockIdx.x;
-  if (task >= L.n_tasks) return;
-  __shared__ WideSmem S;
-  extern __shared__ __align__(16) double wdyn[];  // [J r] chunk / Cholesky panel + block
+// One wide BR-BPNN fit (brbpnn.train) by the whole CTA; `slab` = this CTA's
+// P x P workspace (J'J + factorisation), reused by every fit the CTA runs.
+__device__ __forceinline__ void lm_wide_fit(const WideLaunch& L, int task, double* slab, WideSmem& S,
+                                         double* wdyn) {
   const bbml_lm_task tk = L.tasks[task];
   const int orig = L.orig_index[task];
   const int n = tk.n, d = tk.d, h = tk.h;
@@ -701,7 +701,6 @@ __global__ void __launch_bounds__(WNT) lm_wide_kernel(WideLaunch L) {
   const int ld = L.ld, xs = L.x_stride;
   const double* X = L.X + tk.row_begin * (int64_t)xs;
   const double* Y = L.y + tk.row_begin;
-  double* slab = L.scratch + (int64_t)blockIdx.x * L.slab_doubles;
   double* jtj = slab;
   double* A = jtj + (int64_t)ld * ld;
 
@@ -839,6 +838,27 @@ __global__ void __launch_bounds__(WNT) lm_wide_kernel(WideLaunch L) {
   }
 }
 
+// Persistent grid (one wave of resident CTAs): each CTA pulls the next fit
+// from an atomic counter over the cost-sorted task list and reuses its own
+// slab, so workspace memory is (resident CTAs x slab), not (fits x slab):
+// 160k hidden-64 fits need 148 slabs (~160 MB), not 173 GB, and the fits
+// that early-stop hand their SM to the next one.
+__global__ void __launch_bounds__(WNT) lm_wide_kernel(WideLaunch L) {
+  __shared__ WideSmem S;
+  __shared__ int next;
+  extern __shared__ __align__(16) double wdyn[];  // [J r] chunk / Cholesky panel + block
+  double* slab = L.scratch + (int64_t)blockIdx.x * L.slab_doubles;
+  while (true) {
+    if (threadIdx.x == 0) next = atomicAdd(L.queue, 1);
+    __syncthreads();
+    const int task = next;
+    __syncthreads();
+    if (task >= L.n_tasks) break;
+    lm_wide_fit(L, task, slab, S, wdyn);
+    __syncthreads();
+  }
+}
+
 // Launch all wide tasks (P > 32) of one lm_train call on `s`; tasks/orig are
 // device arrays (already sorted); scratch slabs are stream-ordered.
 bbml_status lm_wide_launch(const bbml_lm_task* d_tasks, const int32_t* d_orig,
@@ -857,7 +877,23 @@ bbml_status lm_wide_launch(const bbml_lm_task* d_tasks, const int32_t* d_orig,
   const int rw = wide_rw(pmax);
   const size_t dyn = (size_t)(WNB * rw + 32 * 33) * sizeof(double);
   (void)nmax;
-  if (alloc_only) return scratch.alloc(slabs, slab * n_tasks);
+  static_assert(WCH == WNB, "chunk rows and panel width share the dynamic buffer");
+  cudaError_t ea = cudaFuncSetAttribute(lm_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)dyn);
+  if (ea != cudaSuccess) return cuda_status(ea, "lm_wide smem");
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lm_wide_kernel, WNT, dyn);
+  const int grid = std::min(n_tasks, std::max(1, per_sm) * sms);
+  // slabs for the resident CTAs, then one double holding the work counter
+  if (alloc_only) {
+    bbml_status st = scratch.alloc(slabs, slab * grid + 1);
+    if (st != BBML_OK) return st;
+    if (cudaMemsetAsync(*slabs + slab * grid, 0, sizeof(double), s) != cudaSuccess)
+      return cuda_status(cudaGetLastError(), "lm_wide queue reset");
+    return BBML_OK;
+  }
   double* d_scratch = *slabs;
   WideLaunch L{};
   L.tasks = d_tasks;
@@ -872,11 +908,8 @@ bbml_status lm_wide_launch(const bbml_lm_task* d_tasks, const int32_t* d_orig,
   L.scratch = d_scratch;
   L.slab_doubles = slab;
   L.ld = ld;
-  static_assert(WCH == WNB, "chunk rows and panel width share the dynamic buffer");
-  cudaError_t ea = cudaFuncSetAttribute(lm_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)dyn);
-  if (ea != cudaSuccess) return cuda_status(ea, "lm_wide smem");
-  lm_wide_kernel<<<n_tasks, WNT, dyn, s>>>(L);
+  L.queue = (int*)(d_scratch + slab * grid);
+  lm_wide_kernel<<<grid, WNT, dyn, s>>>(L);
   cudaError_t e = cudaGetLastError();
 #ifdef BBML_LM_PROF
   {
