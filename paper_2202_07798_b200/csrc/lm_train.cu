@@ -981,8 +981,10 @@ __device__ unsigned long long g_lm_prof[8];
 #endif
 
 // CTAs per SM the register allocation must allow (A/B on sweep / suite16):
-// hidden-1 d <= 2 models are short and numerous -> 6 (80 registers, spills
-// cheaper than the latency they hide); d >= 3 includes the longest series
+// hidden-1 d <= 2 -> 4 (128 registers; r01 measured 6 / 80 registers best
+// with static one-model-per-warp grids, with the persistent warps of r02 the
+// spill-free 4 wins: suite16 FP64 LM call 492 -> 454 ms, step 1 074 -> 1 057
+// ms, tools/r2o.sh); d >= 3 includes the longest series
 // (pathfinder n = 7604), where spills would lengthen the critical chain -> 4
 // PM = 32: 19.5 KB of shared memory per warp (+2 KB static / reserved per
 // CTA).  2-warp CTAs pack 5 x 2 = 10 warps per SM, 3-warp CTAs only 3 x 3;
@@ -994,9 +996,12 @@ __device__ unsigned long long g_lm_prof[8];
 #ifndef LM32_MINB
 #define LM32_MINB 5
 #endif
+#ifndef LM_H1_MINB
+#define LM_H1_MINB 4
+#endif
 template <int PM, int D>
 constexpr int lm_min_blocks() {
-  return PM > 8 ? LM32_MINB : (D == 1 || D == 2) ? 6 : 4;
+  return PM > 8 ? LM32_MINB : (D == 1 || D == 2) ? LM_H1_MINB : 4;
 }
 // NW = 1: one model per warp.  NW > 1 (hidden-1 long series): one model per
 // CTA of NW warps -- the per-sample passes (objective, J'J / J'r) are split

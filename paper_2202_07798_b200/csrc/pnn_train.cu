@@ -1300,7 +1300,10 @@ template <int DM, int SP, typename PermT>
 __global__ void __launch_bounds__(160, 4) pnn_f64_kernel_shared4(PnnLaunch L) {
   pnn_f64_body<DM, SP, PermT>(L);
 }
-// FP64 CTA shapes (development knobs, defaults from one-box A/B):
+// FP64 CTA shapes (development knobs, defaults from one-box A/B; short-series
+// CTAs per SM 3 vs 4: suite16 FP64 step 1 069-1 078 vs 1 092-1 106 ms and
+// 14.9 vs 92 MB of DRAM traffic per PNN call -- the 96-register variant
+// spills, tools/r2r.sh):
 //   BBML_F64_LONG_NPW  = 1 | 2 | 4   producer warps per CTA for n >= kLongSeries
 //   BBML_F64_SHORT_MINB = 3 | 4      CTAs per SM for the shared-producer kernel
 static int env_int(const char* name, int dflt) {
@@ -1324,7 +1327,7 @@ static int f64_short_npw() {
   return v;
 }
 static int f64_short_minb() {
-  static const int v = env_int("BBML_F64_SHORT_MINB", 4);
+  static const int v = env_int("BBML_F64_SHORT_MINB", 3);
   return v;
 }
 
