@@ -50,3 +50,28 @@ def test_reference_arm_world_size_2_rank0_only():
     lines = _json_lines(r.stdout)
     assert len(lines) == 1
     _check(lines[0], 2)
+
+
+def test_strong_scaling_shards_cover_every_unit_once():
+    """bench.py --scaling strong: the fixed (series, restart) unit list is
+    LPT-sharded over the ranks; every unit lands on exactly one rank and the
+    per-rank cost loads are balanced."""
+    import numpy as np
+
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2202_07798_b200 import sharding
+
+    series, spec, kw = bench.workload_series("suite16")
+    for world in (1, 2, 3, 8):
+        shards = [bench.shard_units(series, spec, kw, 4, world, r)[0] for r in range(world)]
+        allu = np.concatenate(shards)
+        assert len(allu) == len(series) * 4
+        assert len({tuple(u) for u in allu.tolist()}) == len(allu)
+        cost = {}
+        for (i, r) in allu.tolist():
+            s = series[i]
+            h = kw["br_hidden"](s.key)
+            cost[(i, r)] = sum(sharding.task_cost(len(s) * 0.7, k, d=s.arity, h=h) for k in ("pnn", "brbpnn"))
+        loads = [sum(cost[tuple(u)] for u in sh.tolist()) for sh in shards]
+        assert max(loads) <= min(loads) + max(cost.values()) + 1e-6  # LPT bound
