@@ -169,7 +169,7 @@ bbml_status bbml_pooled_metrics(const bbml_pred_task* tasks, int32_t n_tasks,
                                 const double* actual_raw, const double* norm, double* out,
                                 void* stream);
 /* Per-model prediction-vs-actual heatmaps (metrics.heatmap_data, metrics.py:145-156):
-   edges (device, bins+1 doubles per task) = linspace(0, max(pred, actual) or 1, bins+1),
+   bins in [2, 200]; edges (device, bins+1 doubles per task) = linspace(0, max(pred, actual) or 1, bins+1),
    counts (device, bins*bins int32 per task, [pred_bin][actual_bin]) of histogram2d. */
 bbml_status bbml_heatmaps(const bbml_pred_task* tasks, int32_t n_tasks, const double* pred,
                           const double* actual_raw, const double* norm, int32_t bins,

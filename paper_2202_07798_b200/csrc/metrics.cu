@@ -270,10 +270,11 @@ static bbml_status segment_metrics(const bbml_pred_task* tasks, int32_t n_tasks,
   if ((st = scratch.upload(d_dst, dst.data(), n_tasks)) != BBML_OK) return st;
   if ((st = scratch.upload(d_segs, segs.data(), n_seg)) != BBML_OK) return st;
   met_gather_kernel<<<n_tasks, MET_NT, 0, stream>>>(d_tasks, d_dst, pred, actual_raw, norm, a, b);
-  if (max_n > 0) {
-    dim3 grid((unsigned)ceil_div(max_n, MET_NT), (unsigned)n_seg);
-    met_rank_kernel<<<grid, MET_NT, 0, stream>>>(d_segs, a, b, ra, rb);
-  }
+  if (max_n > 0)
+    for (int s0 = 0; s0 < n_seg; s0 += 65535) {  // grid.y limit
+      dim3 grid((unsigned)ceil_div(max_n, MET_NT), (unsigned)std::min(65535, n_seg - s0));
+      met_rank_kernel<<<grid, MET_NT, 0, stream>>>(d_segs + s0, a, b, ra, rb);
+    }
   met_corr_kernel<<<n_seg, MET_NT, 0, stream>>>(d_segs, a, b, ra, rb, out);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BBML_OK : cuda_status(e, "segment metrics launch");
@@ -412,8 +413,8 @@ __global__ void __launch_bounds__(MET_NT)
 bbml_status heatmap_launch(const bbml_pred_task* tasks, int32_t n_tasks, const double* pred,
                            const double* actual_raw, const double* norm, int32_t bins,
                            double* edges, int32_t* counts, cudaStream_t stream) {
-  if (bins < 2 || bins > 256) {
-    set_error("bbml_heatmaps: bins=%d outside [2, 256]", bins);
+  if (bins < 2 || bins > 200) {  // bins^2 int counters in shared memory
+    set_error("bbml_heatmaps: bins=%d outside [2, 200]", bins);
     return BBML_ERR_INVALID;
   }
   for (int i = 0; i < n_tasks; ++i) {
