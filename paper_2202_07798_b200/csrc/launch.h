@@ -33,6 +33,9 @@ struct PnnLaunch {
   int32_t stage_off;       // FP64 kernel: byte offset of the row staging area in shared memory
   const double2* bc;       // FP64 kernel: Adam bias corrections {1 - 0.9^t, 1 - 0.999^t}, t = 1..bc_len
   int32_t bc_len;          //   (host libm pow, as the reference's Python float pow); 1.0 beyond
+  const double* rows;      // FP64 kernel: row records [x_0..x_{rec_y-1}, y, pad] (TMA staging)
+  int32_t rec;             //   doubles per record (even: 16-byte multiple)
+  int32_t rec_y;           //   index of y in a record
 };
 
 struct LmLaunch {

@@ -943,12 +943,35 @@ __device__ __forceinline__ void pnn_lat_body(const PnnLaunch& L) {
 //     gradient halves and the updated weights are exchanged with one
 //     xor-16 shuffle per parameter pair.
 // ------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) into shared memory, completion
+// tracked by a per-buffer mbarrier (expected transaction bytes + parity).
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
 
 // pnn.py:184-188 with numpy's rounding, branch-free (f64math.cuh).
 // BC = false: both bias corrections are exactly 1.0 (x / 1.0 == x), so the
@@ -968,15 +991,17 @@ __device__ __forceinline__ void adam_exact(double& p, double& m, double& v, doub
   p = __dsub_rn(p, div_rn_bf(__dmul_rn(lr, mh), __dadd_rn(sqrt_any_bf(vh), 1e-8)));
 }
 
-// staging: per consumer warp, 2 buffers x 2 halves x SP rows x RW doubles
-template <int DM, int SP>
-__host__ __device__ constexpr int f64_stage_doubles() {
-  return 2 * 2 * SP * (DM + 1);
+// staging: per consumer warp, 2 buffers x 2 halves x SP row records of
+// L.rec doubles ([x_0 .. x_{W-1}, y, pad], 16-byte multiple), then 2 mbarriers
+template <int SP>
+__host__ __device__ constexpr int f64_stage_doubles(int rec) {
+  return 2 * 2 * SP * rec + 2;
 }
 
 template <int DM, int SP, typename PermT>
 __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
-  constexpr int RW = DM + 1;  // staged row: x[0..DM), y
+  const int RW = L.rec;       // staged row record: x[0..W), y at W = L.rec_y, pad
+  const int YI = L.rec_y;
   constexpr int C = 2 * SP;   // samples per chunk (both halves)
   constexpr int NP = DM + 2;  // per-unit parameters: w1[0..DM), b1, w2
   const int groups = L.groups_per_cta;
@@ -988,7 +1013,6 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
   int* consumed = SM.consumed;
   PermT* sperm = (PermT*)SM.perm;
   double* stage_all = (double*)(smem_raw + L.stage_off);
-  for (int i = threadIdx.x; i < groups * f64_stage_doubles<DM, SP>(); i += blockDim.x) stage_all[i] = 0.0;
   if (threadIdx.x < groups) {
     produced[threadIdx.x] = 0;
     consumed[threadIdx.x] = 0;
@@ -1005,13 +1029,20 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
   if (gid >= L.n_tasks) return;
   const int sg = lane >> 4, j = lane & 15;
   const unsigned FULL = 0xffffffffu;
-  double* stage = stage_all + gi * f64_stage_doubles<DM, SP>();
+  double* stage = stage_all + gi * f64_stage_doubles<SP>(RW);
+  uint64_t* bars = (uint64_t*)(stage + 2 * 2 * SP * RW);  // one mbarrier per staging buffer
+  if (lane == 0) {
+    mbar_init(bars, 1);
+    mbar_init(bars + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  unsigned parity = 0;  // bit b: phase parity buffer b waits for next
+  int inflight = -1;    // buffer with a bulk copy not yet waited for
 
   const bbml_pnn_task tk = L.tasks[gid];
   const int orig = L.orig_index[gid];
   const int n = tk.n, d = tk.d, h = tk.h, B = tk.batch;
-  const double* __restrict__ X = L.X + tk.row_begin * (int64_t)L.x_stride;
-  const double* __restrict__ Y = L.y + tk.row_begin;
   const PermT* pbase = perm_smem<PermT>() ? sperm + (int64_t)gi * 2 * L.perm_cap
                                       : (const PermT*)L.perm_global + 2 * L.perm_offset[gid];
   const int64_t cap = perm_smem<PermT>() ? L.perm_cap : n;
@@ -1049,21 +1080,25 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
   double fail_value = 0.0;
   const int nbatches = (n + B - 1) / B;
 
-  // lane's staging slots: element e = j and j + 16 of its half's SP x RW block
+  // one TMA bulk copy per row record: lane (sg, j < SP) fetches sample
+  // sg*SP + j of the chunk (samples past the minibatch fetch sample 0's row:
+  // finite, and their d_z is 0); lane 0 posts the chunk's byte count first
+  const double* __restrict__ R = L.rows + tk.row_begin * (int64_t)RW;
+  const unsigned rec_bytes = (unsigned)RW * 8u;
   auto issue = [&](int buf, const PermT* perm, int off, int cnt) {
-    double* dst = stage + (buf * 2 + sg) * SP * RW;
-#pragma unroll
-    for (int rep = 0; rep < 2; ++rep) {
-      const int e = j + 16 * rep;
-      if (e < SP * RW) {
-        const int i = e / RW, k = e % RW;
-        const int c = sg * SP + i;
-        const int row = (int)perm[off + (c < cnt ? c : 0)];
-        if (k < d) cp_async8(dst + e, X + (int64_t)row * L.x_stride + k);
-        else if (k == DM) cp_async8(dst + e, Y + row);
-      }
+    if (lane == 0) mbar_expect_tx(bars + buf, (unsigned)C * rec_bytes);
+    __syncwarp();
+    if (j < SP) {
+      const int c = sg * SP + j;
+      const int row = (int)perm[off + (c < cnt ? c : 0)];
+      tma_bulk_g2s(stage + ((buf * 2 + sg) * SP + j) * RW, R + (int64_t)row * RW, rec_bytes, bars + buf);
     }
-    cp_async_commit();
+    inflight = buf;
+  };
+  auto wait = [&](int buf) {
+    mbar_wait(bars + buf, (parity >> buf) & 1u);
+    parity ^= 1u << buf;
+    if (inflight == buf) inflight = -1;
   };
 
   double g[NP], gb2, bloss;
@@ -1080,6 +1115,7 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
     double eloss = 0.0;
     zero_grads();
     int bs = 0, s0 = 0, buf = 0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     issue(0, perm, 0, min(C, min(B, n)));
     double2 bc = t < L.bc_len ? __ldg(L.bc + t) : make_double2(1.0, 1.0);
     while (true) {
@@ -1091,10 +1127,13 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
         ns0 = 0;
       }
       const bool more = nbs < n;
-      if (more) issue(buf ^ 1, perm, nbs + ns0, min(C, min(B, n - nbs) - ns0));
-      else cp_async_commit();  // empty group keeps wait_group 1 exact
-      cp_async_wait1();
-      __syncwarp();
+      const int cur_inflight = inflight;  // the copy into `buf` (issued one chunk ago)
+      if (more) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of buf^1 before the async overwrite
+        issue(buf ^ 1, perm, nbs + ns0, min(C, min(B, n - nbs) - ns0));
+      }
+      (void)cur_inflight;
+      wait(buf);
       const double* rows = stage + (buf * 2 + sg) * SP * RW;
 
       // forward (own unit, own half's samples)
@@ -1116,7 +1155,7 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
 #pragma unroll
       for (int i = 1; i < SP; ++i)
         if (j == i) zj = z[i];
-      const double yj = j < SP ? rows[j * RW + DM] : 0.5;
+      const double yj = j < SP ? rows[j * RW + YI] : 0.5;
       const bool mine = j < SP && (sg * SP + j) < cnt;
       const double nb_t = (double)nb;
       const double zz = __dadd_rn(zj, b2);
@@ -1260,7 +1299,7 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
       st_volatile(consumed + gi, ep + 1);
     }
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (inflight >= 0) wait(inflight);  // a run that stopped early leaves no copy in flight
   if (lane == 0) st_volatile(consumed + gi, kConsumedDone);
 
   double* W = L.weights + tk.w_offset;
@@ -1377,6 +1416,19 @@ __global__ void to_float_kernel(const double* __restrict__ X, int xs, float* __r
   }
 }
 
+// FP64 row records for the TMA staging: [x_0 .. x_{W-1} (zero past
+// x_stride), y, zero pad] with W = rec_y, rec = W + 1 rounded up to an even
+// count (16-byte multiple, the bulk-copy granularity).
+__global__ void to_records_kernel(const double* __restrict__ X, int xs, const double* __restrict__ y,
+                                  int rec_y, int rec, double* __restrict__ out, int64_t rows) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * rec;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / rec;
+    const int k = (int)(e - r * rec);
+    out[e] = k < xs ? X[r * xs + k] : k == rec_y ? y[r] : 0.0;
+  }
+}
+
 static int bucket_d(int d) { return d <= 2 ? 2 : d <= 4 ? 4 : 16; }
 static int bucket_h(int h) { return h <= 16 ? 16 : 64; }
 // series at least this long get a dedicated producer warp (see launch_variant)
@@ -1434,7 +1486,7 @@ static cudaError_t launch_variant(PnnLaunch L, int64_t nmax, size_t smem_limit, 
   constexpr bool F64 = LAT && sizeof(T) == 8;
   if (F64) {  // per-warp row staging after the permutation buffers
     L.stage_off = (int32_t)(16 * ((smem + 15) / 16));
-    smem = L.stage_off + (size_t)groups * f64_stage_doubles<DM, 5>() * sizeof(double);
+    smem = L.stage_off + (size_t)groups * f64_stage_doubles<5>(L.rec) * sizeof(double);
   }
   auto k = !LAT ? pnn_train_kernel<T, DM, HM, G, SC, PermT>
                 : F64 ? (shared_prod ? (f64_short_minb() == 4 ? pnn_f64_kernel_shared4<DM, 5, PermT>
@@ -1573,6 +1625,24 @@ bbml_status pnn_train_launch(const bbml_pnn_task* tasks, int32_t n_tasks, const 
     to_float_kernel<<<(int)std::min<int64_t>(ceil_div(rows, 256), 4096), 256, 0, stream>>>(
         X, x_stride, d_xf, xf_stride, y, d_yf, rows);
   }
+  // FP64: 16-byte-multiple row records for the TMA staging (see pnn_f64_body)
+  double* d_rec = nullptr;
+  int rec_y = 0, rec = 0;
+  if (precision == 64) {
+    int dmax = 1;
+    int64_t rows = 0;
+    for (int i = 0; i < n_tasks; ++i) {
+      dmax = std::max(dmax, sorted[i].d);
+      rows = std::max<int64_t>(rows, sorted[i].row_begin + sorted[i].n);
+    }
+    rec_y = std::max(x_stride, bucket_d(dmax));  // every bucket's DM <= rec_y
+    rec = (rec_y + 2) & ~1;
+    if ((st = scratch.alloc(&d_rec, std::max<int64_t>(rows, 1) * rec)) != BBML_OK) return st;
+    const int64_t tot = rows * rec;
+    if (tot > 0)
+      to_records_kernel<<<(int)std::min<int64_t>(ceil_div(tot, 256), 4096), 256, 0, stream>>>(
+          X, x_stride, y, rec_y, rec, d_rec, rows);
+  }
   // FP64: Adam bias-correction table (see pnn_f64_body)
   double2* d_bc = nullptr;
   const std::vector<double2>& bc_host = adam_bias_table();
@@ -1637,6 +1707,9 @@ bbml_status pnn_train_launch(const bbml_pnn_task* tasks, int32_t n_tasks, const 
     L.poll_cap_ns = precision == 64 ? 2000 : 100;
     L.bc = d_bc;
     L.bc_len = precision == 64 ? (int32_t)bc_host.size() : 0;
+    L.rows = d_rec;
+    L.rec = rec;
+    L.rec_y = rec_y;
     cudaError_t e = precision == 32 ? launch_bucket<float>(dm, hm, L, nmax, smem_limit, stream)
                                     : launch_bucket<double>(dm, hm, L, nmax, smem_limit, stream);
     if (e != cudaSuccess) return cuda_status(e, "pnn_train launch");
