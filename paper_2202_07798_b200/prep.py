@@ -110,9 +110,13 @@ def split_labels(t: SeriesTable, mode: str, fraction: float, seed: int):
         # padded columns get theta = +inf for LOW (x <= inf) and -inf for
         # HIGH (x > -inf), so the row-wise all() only sees the series' own
         theta = lo + fraction * (hi - lo)
-        rs = np.repeat(np.arange(len(t.keys)), n)
-        low = (t.X <= np.where(own, theta, np.inf)[rs]).all(axis=1)
-        high = (t.X > np.where(own, theta, -np.inf)[rs]).all(axis=1)
+        tlo = np.repeat(np.where(own, theta, np.inf), n, axis=0)
+        thi = np.repeat(np.where(own, theta, -np.inf), n, axis=0)
+        low = t.X[:, 0] <= tlo[:, 0]
+        high = t.X[:, 0] > thi[:, 0]
+        for k in range(1, t.X.shape[1]):  # column-wise all(): D <= 16 passes
+            low &= t.X[:, k] <= tlo[:, k]
+            high &= t.X[:, k] > thi[:, k]
         labels[high] = TEST
         if mode == "high-low":
             labels[low & ~high] = TRAIN
@@ -121,8 +125,13 @@ def split_labels(t: SeriesTable, mode: str, fraction: float, seed: int):
         else:
             raise ValueError(f"unknown split mode {mode!r}")
     S = len(t.keys)
-    rs = np.repeat(np.arange(S), n)
-    counts = np.bincount(rs * 3 + labels, minlength=3 * S).reshape(S, 3)
+    # per-series label counts: prefix sums of the train / test indicators at the segment ends
+    ends = t.offsets
+    ctr = np.concatenate([[0], np.cumsum(labels == TRAIN)])[ends]
+    cte = np.concatenate([[0], np.cumsum(labels == TEST)])[ends]
+    counts = np.zeros((S, 3), dtype=np.int64)
+    counts[:, TRAIN] = np.diff(ctr)
+    counts[:, TEST] = np.diff(cte)
     for s in np.flatnonzero((counts[:, TRAIN] == 0) | (counts[:, TEST] == 0)):
         s = int(s)
         if s not in errors:
