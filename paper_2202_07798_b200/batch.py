@@ -104,11 +104,11 @@ def build_workload(series: Sequence[BbSeries], spec: SplitSpec, *, kinds=("pnn",
     d_ser = np.where(ok_mask, t.d, 0).astype(np.int32)
     train = engine.Packed(P.Xtr, P.ytr, P.tr_off[:-1].copy(), np.diff(P.tr_off).astype(np.int32), t.d.copy())
     test = engine.Packed(P.Xte, P.yte, P.te_off[:-1].copy(), np.diff(P.te_off).astype(np.int32), t.d.copy())
-    norms = [None if not ok_mask[i] else
-             Normalizer(P.x_min[i, :t.d[i]].copy(), P.x_max[i, :t.d[i]].copy(), float(P.y_min[i]),
-                        float(P.y_max[i])) for i in range(S)]
+    norms = _Normalizers(P, ok_mask)
     ok = P.ok.astype(np.int64)
-    app_crc = np.array([zlib.crc32(k[0].encode("utf-8")) for k in keys], dtype=np.uint64)
+    crc = {}
+    app_crc = np.array([crc.setdefault(k[0], zlib.crc32(k[0].encode("utf-8"))) for k in keys],
+                       dtype=np.uint64)
     kid = np.array([k[1] for k in keys], dtype=np.uint64)
     bid = np.array([k[2] for k in keys], dtype=np.uint64)
     tabs = {}
@@ -141,8 +141,11 @@ def build_workload(series: Sequence[BbSeries], spec: SplitSpec, *, kinds=("pnn",
             tab, Pn = engine.pnn_tasks(rb, n, d, pnn_hidden, pnn_epochs, pnn_batch, pnn_lr, 1e-8,
                                        seeds, False)
         else:
-            h = (np.array([br_hidden(keys[i]) for i in sidx], dtype=np.int32)
-                 if callable(br_hidden) else br_hidden)
+            if callable(br_hidden):  # once per series, then gathered per task
+                hs = np.array([br_hidden(k) for k in keys], dtype=np.int32)
+                h = hs[sidx]
+            else:
+                h = br_hidden
             tab, Pn = engine.lm_tasks(rb, n, d, h, br_max_epochs, seeds, False)
         tabs[kind] = (tab, Pn, sidx)
     empty_p = np.zeros(0, dtype=_lib.PNN_TASK)
@@ -155,6 +158,27 @@ def build_workload(series: Sequence[BbSeries], spec: SplitSpec, *, kinds=("pnn",
                   np.zeros(0, np.int64) if lt is None else lP, precision, P.errors, P.yte_raw)
     wl._norm_rows = P.norm_rows(dmax)
     return wl
+
+
+class _Normalizers:
+    """Per-series ``Normalizer`` views of the batched statistics, built on
+    access (None for series that failed to split)."""
+
+    def __init__(self, P, ok_mask):
+        self._P, self._ok = P, ok_mask
+
+    def __len__(self) -> int:
+        return len(self._ok)
+
+    def __getitem__(self, i):
+        if not self._ok[i]:
+            return None
+        P, d = self._P, int(self._P.table.d[i])
+        return Normalizer(P.x_min[i, :d].copy(), P.x_max[i, :d].copy(), float(P.y_min[i]),
+                          float(P.y_max[i]))
+
+    def __iter__(self):
+        return (self[i] for i in range(len(self)))
 
 
 class DeviceWorkload:

@@ -55,9 +55,12 @@ class SeriesTable:
         off = np.zeros(len(series) + 1, dtype=np.int64)
         np.cumsum(n, out=off[1:])
         dmax = int(d.max(initial=1))
-        X = np.zeros((int(off[-1]), dmax))
-        for s, (a, b) in zip(series, zip(off[:-1], off[1:])):
-            X[a:b, :s.X.shape[1]] = s.X
+        if len(series) and (d == dmax).all():  # one arity: a single concatenation
+            X = np.concatenate([np.asarray(s.X, dtype=float) for s in series]).reshape(-1, dmax)
+        else:
+            X = np.zeros((int(off[-1]), dmax))
+            for s, (a, b) in zip(series, zip(off[:-1], off[1:])):
+                X[a:b, :s.X.shape[1]] = s.X
         y = np.concatenate([np.asarray(s.y, dtype=float) for s in series]) if len(series) else np.zeros(0)
         return cls([s.key for s in series], X, y, off, d)
 
