@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include "../../include/bbml.h"
+#include "f64math.cuh"
 
 namespace bbml {
 
@@ -48,9 +49,22 @@ __device__ __forceinline__ float tanh_fast(float x) {
   return ax < 0.125f ? poly : copysignf(big, x);
 }
 
-// brbpnn.tansig (brbpnn.py:33-38): 2/(1+exp(-2x)) - 1, saturating.
+// brbpnn.tansig (brbpnn.py:33-38): 2/(1+exp(-2x)) - 1, saturating, with the
+// branch-free (bit-identical) division of f64math.cuh, so the per-sample
+// loops of the LM kernels overlap more of consecutive samples' tansig chains.
+// BBML_TANSIG_EXP_BF also swaps exp for the branch-free one (within 1 ulp of
+// libdevice: LM call 455 -> 428 ms on suite16, but the near-chaotic BR fits
+// then move by more than the artifact test's tolerance -- not the default).
 __device__ __forceinline__ double tansig(double x) {
-  return __dsub_rn(__ddiv_rn(2.0, __dadd_rn(1.0, exp(-2.0 * x))), 1.0);
+#ifdef BBML_TANSIG_EXP_BF
+  const double t = __dsub_rn(div_rn_bf(2.0, __dadd_rn(1.0, exp_any_bf(-2.0 * x))), 1.0);
+  return x != x ? x : t;
+#else
+  // exp from libdevice (bit-identical results to r01), division branch-free
+  const double e = exp(-2.0 * x);
+  const double t = __dsub_rn(div_rn_bf(2.0, __dadd_rn(1.0, e)), 1.0);
+  return e == INFINITY ? -1.0 : t;  // 2 / inf = 0 exactly in IEEE; div_rn_bf(2, inf) is not
+#endif
 }
 
 __device__ __forceinline__ double shfl_xor(double v, int m, unsigned mask = 0xffffffffu,
