@@ -608,7 +608,7 @@ __device__ bool w_solve(WarpLm<PM>& S, int P, double alpha, double beta, double 
     }
     __syncwarp();
     if (lane > k && lane < P) {
-      const double l = __ddiv_rn(S.A[lane * LD + k], S.A[k * LD + k]);
+      const double l = div_safe_bf(S.A[lane * LD + k], S.A[k * LD + k]);
       S.A[lane * LD + k] = l;
       for (int j = k + 1; j < P; ++j) S.A[lane * LD + j] = fma(-l, S.A[k * LD + j], S.A[lane * LD + j]);
     }
@@ -625,7 +625,7 @@ __device__ bool w_solve(WarpLm<PM>& S, int P, double alpha, double beta, double 
     double s = 0.0;
     for (int j = i + 1 + lane; j < P; j += 32) s = fma(S.A[i * LD + j], S.delta[j], s);
     s = warp_sum(s);
-    if (lane == 0) S.delta[i] = __ddiv_rn(__dsub_rn(S.rhs[i], s), S.A[i * LD + i]);
+    if (lane == 0) S.delta[i] = div_safe_bf(__dsub_rn(S.rhs[i], s), S.A[i * LD + i]);
     __syncwarp();
   }
   return true;
@@ -801,10 +801,12 @@ __device__ double w_gamma(WarpLm<PM>& S, int P, double alpha, double beta, int l
         double c = 1.0, s = 0.0;
         if (q < P) {
           const double apq = S.A[p * LD + q], app = S.A[p * LD + p], aqq = S.A[q * LD + q];
-          if (fabs(apq) > floor_abs && fabs(apq) > 1e-15 * sqrt(fabs(app * aqq))) {
-            const double tau = (aqq - app) / (2.0 * apq);
-            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-            c = 1.0 / sqrt(1.0 + t * t);
+          // same arithmetic with the branch-free correctly-rounded division and
+          // square root (f64math.cuh): identical values, no branch per operation
+          if (fabs(apq) > floor_abs && fabs(apq) > 1e-15 * sqrt_nonneg_bf(fabs(app * aqq))) {
+            const double tau = div_safe_bf(aqq - app, 2.0 * apq);
+            const double t = div_safe_bf(tau >= 0.0 ? 1.0 : -1.0, fabs(tau) + sqrt_nonneg_bf(1.0 + tau * tau));
+            c = div_rn_bf(1.0, sqrt_rn_bf(1.0 + t * t));
             s = t * c;
             rot = true;
           }

@@ -976,11 +976,7 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigne
 // pnn.py:184-188 with numpy's rounding, branch-free (f64math.cuh).
 // BC = false: both bias corrections are exactly 1.0 (x / 1.0 == x), so the
 // two divisions by them are dropped.
-__device__ __forceinline__ double sqrt_any_bf(double x) {  // x >= 0, denormals included
-  const bool tiny = x < 0x1p-968;
-  const double s = sqrt_rn_bf(tiny ? x * 0x1p1000 : x);  // exact power-of-4 scaling
-  return tiny ? s * 0x1p-500 : s;
-}
+__device__ __forceinline__ double sqrt_any_bf(double x) { return sqrt_nonneg_bf(x); }
 template <bool BC>
 __device__ __forceinline__ void adam_exact(double& p, double& m, double& v, double g, double bc1,
                                            double bc2, double lr) {
