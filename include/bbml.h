@@ -13,6 +13,7 @@
  *   bbml_metrics      <- bbcount/metrics.py:33-76    mse / pearson / spearman
  *   bbml_pooled_metrics <- bbcount/experiment.py:180-206 pooled per-app correlations
  *   bbml_heatmaps     <- bbcount/metrics.py:145-156  heatmap_data (experiment.py:417-424)
+ *   bbml_kde          <- bbcount/metrics.py:95-118   kde (experiment.py:425-430)
  *                        bbcount/brbpnn.py:85-91     brbpnn.forward
  *                        bbcount/persist.py:35-43    SavedModel.predict_normalized / predict_counts
  *   bbml_pnn_loss_grad<- bbcount/pnn.py:121-147      pnn.loss_and_grads (unit level)
@@ -174,6 +175,14 @@ bbml_status bbml_pooled_metrics(const bbml_pred_task* tasks, int32_t n_tasks,
 bbml_status bbml_heatmaps(const bbml_pred_task* tasks, int32_t n_tasks, const double* pred,
                           const double* actual_raw, const double* norm, int32_t bins,
                           double* edges, int32_t* counts, void* stream);
+
+/* Per-series count KDE (metrics.kde, metrics.py:95-118): series i = values[offsets[i] ..
+   offsets[i+1]) (offsets: HOST, n_series + 1; values: device).  Out (device): grid and density
+   (grid_points doubles per series) and the Scott bandwidth; bandwidth 0 = no curve (zero
+   spread or n < 2, where the reference raises BandwidthError). */
+bbml_status bbml_kde(const int64_t* offsets, int32_t n_series, const double* values,
+                     int32_t grid_points, double* grid, double* density, double* bandwidth,
+                     void* stream);
 
 /* ---- unit-level kernels (one model per task; rows at row_begin, n rows) ---- */
 /* loss[i] and grads (P doubles at w_offset of grads) of the batch NLL */

@@ -50,7 +50,7 @@ EXPORTS = (
     "bbml_seedseq_generate", "bbml_pcg64_state", "bbml_pnn_train", "bbml_lm_train",
     "bbml_predict", "bbml_pnn_loss_grad", "bbml_lm_jacobian", "bbml_lm_solve",
     "bbml_lm_evidence", "bbml_lm_gram", "bbml_adam_step", "bbml_tansig",
-    "bbml_fma_peak", "bbml_metrics", "bbml_pooled_metrics", "bbml_heatmaps",
+    "bbml_fma_peak", "bbml_metrics", "bbml_pooled_metrics", "bbml_heatmaps", "bbml_kde",
 )
 
 
@@ -83,6 +83,7 @@ _SIGS = {
     "bbml_metrics": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "bbml_pooled_metrics": (_i32, [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp]),
     "bbml_heatmaps": (_i32, [_vp, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
+    "bbml_kde": (_i32, [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp]),
     "bbml_pnn_loss_grad": (_i32, [_vp, _i32, _vp, _vp, _i32, _vp, _f64, _vp, _vp, _vp]),
     "bbml_lm_jacobian": (_i32, [_vp, _i32, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "bbml_lm_gram": (_i32, [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

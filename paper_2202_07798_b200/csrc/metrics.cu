@@ -458,6 +458,124 @@ extern "C" bbml_status bbml_metrics(const bbml_pred_task* tasks, int32_t n_tasks
                         (cudaStream_t)stream);
 }
 
+namespace bbml {
+
+// ---------------------------------------------------------------------------
+// Per-series count KDE (metrics.kde, metrics.py:95-118, one curve per series
+// in run_experiment): Scott bandwidth n^(-1/5) * std(ddof = 1), grid =
+// linspace(min - 3 bw, max + 3 bw, G), density = sum exp(-z^2 / 2) /
+// (n bw sqrt(2 pi)).  One CTA per series: block reductions for mean / spread /
+// range, then one grid point per thread over the series' counts staged in
+// shared memory.  bw = 0 (no spread, n < 2) marks "no curve" (the reference
+// raises BandwidthError and skips the file).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(MET_NT)
+    kde_kernel(const int64_t* __restrict__ off, const double* __restrict__ vals, int G, int cap,
+               double* __restrict__ grid_out, double* __restrict__ dens_out, double* __restrict__ bw_out) {
+  extern __shared__ __align__(16) double kx[];
+  __shared__ double red[MET_NT / 32];
+  const int64_t a = off[blockIdx.x], n = off[blockIdx.x + 1] - a;
+  double* go = grid_out + (int64_t)blockIdx.x * G;
+  double* dout = dens_out + (int64_t)blockIdx.x * G;
+  double sum = 0.0, lo = __longlong_as_double(0x7ff0000000000000LL), hi = -lo;
+  for (int64_t i = threadIdx.x; i < n; i += MET_NT) {
+    const double v = vals[a + i];
+    if (i < cap) kx[i] = v;
+    sum += v;
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+  }
+  const double mean = met_sum(sum, red) / (double)n;
+  double ss = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += MET_NT) {
+    const double dv = vals[a + i] - mean;
+    ss = fma(dv, dv, ss);
+  }
+  const double var = n > 1 ? met_sum(ss, red) / (double)(n - 1) : 0.0;
+  // block min / max
+  for (int o = 16; o >= 1; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = lo;
+  __syncthreads();
+  double blo = red[0];
+  for (int w = 1; w < MET_NT / 32; ++w) blo = fmin(blo, red[w]);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = hi;
+  __syncthreads();
+  double bhi = red[0];
+  for (int w = 1; w < MET_NT / 32; ++w) bhi = fmax(bhi, red[w]);
+  const double spread = sqrt(var);
+  if (!(spread > 0.0)) {
+    if (threadIdx.x == 0) bw_out[blockIdx.x] = 0.0;
+    return;
+  }
+  // numpy's rounding order (no contraction): linspace = g * step + start,
+  // z = (x - v) / bw, exp(-0.5 * z**2)
+  const double bw = __dmul_rn(pow((double)n, -1.0 / 5.0), spread);
+  const double g0 = __dsub_rn(blo, __dmul_rn(3.0, bw)), g1 = __dadd_rn(bhi, __dmul_rn(3.0, bw));
+  const double step = __ddiv_rn(__dsub_rn(g1, g0), (double)(G - 1));
+  const double norm = __dmul_rn(__dmul_rn((double)n, bw), 2.5066282746310002);  // sqrt(2 pi)
+  for (int g = threadIdx.x; g < G; g += MET_NT) {
+    const double x = g == G - 1 ? g1 : __dadd_rn(__dmul_rn((double)g, step), g0);
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      const double z = __ddiv_rn(__dsub_rn(x, i < cap ? kx[i] : vals[a + i]), bw);
+      acc += exp(__dmul_rn(-0.5, __dmul_rn(z, z)));
+    }
+    go[g] = x;
+    dout[g] = __ddiv_rn(acc, norm);
+  }
+  if (threadIdx.x == 0) bw_out[blockIdx.x] = bw;
+}
+
+bbml_status kde_launch(const int64_t* off, int32_t n_series, const double* vals, int32_t G,
+                       double* grid, double* dens, double* bw, cudaStream_t stream) {
+  if (G < 2) {
+    set_error("bbml_kde: grid_points=%d < 2", G);
+    return BBML_ERR_INVALID;
+  }
+  if (n_series == 0) return BBML_OK;
+  int64_t max_n = 0;
+  for (int i = 0; i < n_series; ++i) {
+    if (off[i + 1] < off[i]) {
+      set_error("bbml_kde: offsets not monotone at %d", i);
+      return BBML_ERR_INVALID;
+    }
+    max_n = std::max<int64_t>(max_n, off[i + 1] - off[i]);
+  }
+  ScratchBuffer scratch(stream);
+  int64_t* d_off = nullptr;
+  bbml_status st;
+  if ((st = scratch.alloc(&d_off, n_series + 1)) != BBML_OK) return st;
+  if ((st = scratch.upload(d_off, off, n_series + 1)) != BBML_OK) return st;
+  const int cap = (int)std::min<int64_t>(max_n, 12288);  // counts staged in shared memory (96 KB)
+  const size_t smem = (size_t)std::max(cap, 1) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(kde_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_status(e, "kde smem");
+  kde_kernel<<<n_series, MET_NT, smem, stream>>>(d_off, vals, G, cap, grid, dens, bw);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_status(e, "kde launch");
+  return scratch.release();
+}
+
+}  // namespace bbml
+
+extern "C" bbml_status bbml_kde(const int64_t* offsets, int32_t n_series, const double* values,
+                                int32_t grid_points, double* grid, double* density, double* bandwidth,
+                                void* stream) {
+  using namespace bbml;
+  if (n_series == 0) return BBML_OK;
+  if (!offsets || !values || !grid || !density || !bandwidth || n_series < 0) {
+    set_error("bbml_kde: NULL argument or n_series < 0");
+    return BBML_ERR_INVALID;
+  }
+  return kde_launch(offsets, n_series, values, grid_points, grid, density, bandwidth,
+                    (cudaStream_t)stream);
+}
+
 extern "C" bbml_status bbml_pooled_metrics(const bbml_pred_task* tasks, int32_t n_tasks,
                                            const int32_t* seg_of, int32_t n_seg, const double* pred,
                                            const double* actual_raw, const double* norm,

@@ -342,3 +342,26 @@ def heatmaps(pred, actual_raw, pred_offset, row_begin, n, d, norms, bins, device
                               _stream(torch)), "bbml_heatmaps")
     return (edges.cpu().numpy()[:M * (bins + 1)].reshape(M, bins + 1),
             counts.cpu().numpy()[:M * bins * bins].reshape(M, bins, bins))
+
+
+def kde(values: Sequence[np.ndarray], grid_points: int = 256, device=None):
+    """Count KDE of many series on the device (``bbml_kde``): returns
+    (grid (S, G), density (S, G), bandwidth (S,)) host arrays; bandwidth 0
+    where the series has no spread (no curve)."""
+    torch = torch_cuda()
+    dev = torch.device("cuda" if device is None else device)
+    n = np.array([len(v) for v in values], dtype=np.int64)
+    off = np.zeros(len(values) + 1, dtype=np.int64)
+    np.cumsum(n, out=off[1:])
+    S = len(values)
+    if S == 0:
+        return np.zeros((0, grid_points)), np.zeros((0, grid_points)), np.zeros(0)
+    flat = np.concatenate([np.asarray(v, dtype=np.float64) for v in values]) if off[-1] else np.zeros(1)
+    vd = torch.from_numpy(flat).to(dev)
+    grid = torch.empty(S * grid_points, dtype=torch.float64, device=dev)
+    dens = torch.empty(S * grid_points, dtype=torch.float64, device=dev)
+    bw = torch.empty(S, dtype=torch.float64, device=dev)
+    check(lib().bbml_kde(ptr(off), S, ptr(vd), int(grid_points), ptr(grid), ptr(dens), ptr(bw),
+                         _stream(torch)), "bbml_kde")
+    return (grid.cpu().numpy().reshape(S, grid_points), dens.cpu().numpy().reshape(S, grid_points),
+            bw.cpu().numpy())

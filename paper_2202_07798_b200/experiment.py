@@ -338,6 +338,7 @@ def train_many(pairs: Sequence[tuple], config: ExperimentConfig, *, precision: O
                     "gamma": float(st["gamma"]) if ran else None,
                     "mu": float(st["mu"]) if ran else None}
         res.saved = SavedModel(kind, model, t.prep.norm, t.prep.series.key, seed, meta)
+        res.saved._packed = w  # pack-order weights (columnar writer)
     return BatchOutput(results, dev_s, launches)
 
 
@@ -550,6 +551,23 @@ def write_split_manifests(series_list: Sequence[BbSeries], spec: SplitSpec, out_
             fh.write("\n".join(lines) + "\n")
 
 
+def write_splits_columnar(series_list: Sequence[BbSeries], spec: SplitSpec, path: Path) -> None:
+    """The splits manifest as arrays (columnar layout): per series its key
+    and row range (CSR offsets into the input trace rows, in input order),
+    per row its partition code (0 discarded, 1 train, 2 test, -1 the
+    series' range split failed: the reference's ``error`` label)."""
+    table = prep.SeriesTable.from_series(series_list)
+    labels, errors = prep.split_labels(table, spec.mode.value, spec.fraction, spec.seed)
+    lab = labels.astype(np.int8)
+    for i, msg in errors.items():
+        if "are constant" in msg:
+            lab[table.offsets[i]:table.offsets[i + 1]] = -1
+    np.savez(path, app=np.array([k[0] for k in table.keys]).astype(str),
+             kernel_id=np.array([k[1] for k in table.keys], dtype=np.int64),
+             bb_id=np.array([k[2] for k in table.keys], dtype=np.int64), offsets=table.offsets,
+             partition=lab)
+
+
 def device_heatmaps(rows: Sequence[SeriesResult], bins: int):
     """Heatmap edges / counts of every successful row in one device call
     (bbml_heatmaps); returns (row indices, edges (M, bins+1), counts (M, bins, bins))."""
@@ -567,31 +585,81 @@ def device_heatmaps(rows: Sequence[SeriesResult], bins: int):
     return idx, edges, counts
 
 
+_CFG_NUMERIC = ("epochs_run", "gamma", "mu")  # per-model BR values, kept as columns
+
+
 def write_models_columnar(rows: Sequence[SeriesResult], path: Path) -> int:
     """Every saved model of a run in ONE columnar file (numpy .npz): keys,
     kinds, shapes, seeds, flat pack-order weights + offsets, normalisers,
-    BR hyperparameters and per-model config JSON.  ``export_models_json``
-    turns it into the reference's per-model JSON (schema v1) files."""
+    BR hyperparameters, the per-model config as a shared JSON template plus
+    numeric columns.  ``export_models_json`` turns it into the reference's
+    per-model JSON (schema v1) files."""
     saved = [r.saved for r in rows if r.saved is not None]
     M = len(saved)
-    d = np.array([m.model.n_inputs for m in saved], dtype=np.int32)
-    h = np.array([m.model.hidden for m in saved], dtype=np.int32)
-    w = [np.concatenate([np.ravel(m.model.W1), m.model.b1, m.model.W2, [m.model.b2]]) for m in saved]
+    models = [m.model for m in saved]
+    d = np.fromiter((m.n_inputs for m in models), dtype=np.int32, count=M)
+    h = np.fromiter((m.hidden for m in models), dtype=np.int32, count=M)
+    w = [getattr(m, "_packed", None) for m in saved]
+    w = [x if x is not None else np.concatenate([np.ravel(mm.W1), mm.b1, mm.W2, [mm.b2]])
+         for x, mm in zip(w, models)]
     D = max(1, int(d.max())) if M else 1
+    norm = np.zeros((M, 2 * D + 2))
+    for i, m in enumerate(saved):  # [x_min(d), x_max(d), y_min, y_max]
+        nm, di = m.normalizer, int(d[i])
+        norm[i, :di] = nm.x_min
+        norm[i, di:2 * di] = nm.x_max
+        norm[i, 2 * di] = nm.y_min
+        norm[i, 2 * di + 1] = nm.y_max
+    templates: dict = {}
+    tpl = np.zeros(M, dtype=np.int32)
+    num = np.full((M, len(_CFG_NUMERIC)), np.nan)
+    isnone = np.zeros((M, len(_CFG_NUMERIC)), dtype=bool)
+    for i, m in enumerate(saved):
+        cfg = m.config
+        key = tuple((k, None if k in _CFG_NUMERIC else v) for k, v in cfg.items())
+        tpl[i] = templates.setdefault(key, len(templates))
+        for c, k in enumerate(_CFG_NUMERIC):
+            if k in cfg:
+                v = cfg[k]
+                if v is None:
+                    isnone[i, c] = True
+                else:
+                    num[i, c] = v
+    tpl_json = [json.dumps(dict(k)) for k in sorted(templates, key=templates.get)]
     np.savez(path,
-             app=np.array([m.key[0] for m in saved], dtype=object).astype(str),
-             kernel_id=np.array([m.key[1] for m in saved], dtype=np.int64),
-             bb_id=np.array([m.key[2] for m in saved], dtype=np.int64),
+             app=np.array([m.key[0] for m in saved]).astype(str),
+             kernel_id=np.fromiter((m.key[1] for m in saved), dtype=np.int64, count=M),
+             bb_id=np.fromiter((m.key[2] for m in saved), dtype=np.int64, count=M),
              kind=np.array([m.kind for m in saved]).astype(str), d=d, h=h,
              seed=np.array([str(m.seed) for m in saved]).astype(str),
              weights=np.concatenate(w) if w else np.zeros(0),
              w_offset=engine.offsets(np.array([len(x) for x in w], dtype=np.int64)) if M else np.zeros(0, np.int64),
-             norm=np.stack([m.normalizer.row(D) for m in saved]) if M else np.zeros((0, 2 * D + 2)),
-             eps=np.array([getattr(m.model, "eps", np.nan) for m in saved]),
-             alpha=np.array([getattr(m.model, "alpha", np.nan) for m in saved]),
-             beta=np.array([getattr(m.model, "beta", np.nan) for m in saved]),
-             config=np.array([json.dumps(m.config) for m in saved]).astype(str))
+             norm=norm,
+             eps=np.fromiter((getattr(m, "eps", np.nan) for m in models), dtype=np.float64, count=M),
+             alpha=np.fromiter((getattr(m, "alpha", np.nan) for m in models), dtype=np.float64, count=M),
+             beta=np.fromiter((getattr(m, "beta", np.nan) for m in models), dtype=np.float64, count=M),
+             config_template=np.array(tpl_json).astype(str), config_index=tpl,
+             config_numeric=num, config_none=isnone,
+             config_int=np.array([k in ("epochs_run",) for k in _CFG_NUMERIC]))
     return M
+
+
+def read_kde_columnar(path: Union[str, Path]) -> dict:
+    """{slug: KdeCurve} from kde.npz (grid rebuilt as linspace(lo, hi, G))."""
+    z = np.load(path, allow_pickle=False)
+    G = z["density"].shape[1] if z["density"].ndim == 2 else 256
+    return {str(s): metrics.KdeCurve(np.linspace(z["lo"][i], z["hi"][i], G), z["density"][i],
+                                     float(z["bandwidth"][i])) for i, s in enumerate(z["slug"])}
+
+
+def read_heatmaps_columnar(path: Union[str, Path]) -> dict:
+    """{slug: HeatmapData} from heatmaps.npz (sparse counts back to bins x bins)."""
+    z = np.load(path, allow_pickle=False)
+    B = int(z["bins"])
+    counts = np.zeros((len(z["slug"]), B * B), dtype=np.int64)
+    counts[z["model"], z["bin"]] = z["count"]
+    return {str(s): metrics.HeatmapData(z["edges"][i], counts[i].reshape(B, B))
+            for i, s in enumerate(z["slug"])}
 
 
 def read_models_columnar(path: Union[str, Path]) -> list:
@@ -609,7 +677,12 @@ def read_models_columnar(path: Union[str, Path]) -> list:
         row = z["norm"][i]
         norm = Normalizer(row[:d].copy(), row[d:2 * d].copy(), float(row[2 * d]), float(row[2 * d + 1]))
         key = (str(z["app"][i]), int(z["kernel_id"][i]), int(z["bb_id"][i]))
-        out.append(SavedModel(kind, model, norm, key, int(z["seed"][i]), json.loads(str(z["config"][i]))))
+        cfg = json.loads(str(z["config_template"][int(z["config_index"][i])]))
+        for c, k in enumerate(_CFG_NUMERIC):
+            if k in cfg:
+                v = z["config_numeric"][i, c]
+                cfg[k] = None if z["config_none"][i, c] else (int(v) if z["config_int"][c] else float(v))
+        out.append(SavedModel(kind, model, norm, key, int(z["seed"][i]), cfg))
     return out
 
 
@@ -647,32 +720,56 @@ def run_experiment(series_list: Sequence[BbSeries], config: ExperimentConfig,
     ``layout="files"`` writes the reference's artifact tree (report.csv,
     summary.csv, splits_<app>.csv, models/<slug>.json, heatmap_<slug>.csv,
     kde_<slug>.csv, manifest.json).  ``layout="columnar"`` keeps report /
-    summary / splits / manifest and replaces the per-model files with
+    summary / manifest and replaces the per-model / per-series files with
     models.npz, heatmaps.npz and kde.npz (one file each however many models:
-    cfg 4 has 320k of them); ``export_models_json`` recovers the JSON files.
+    cfg 4 has 320k of them) and splits_<app>.csv with splits.npz (per-row
+    partition codes); ``export_models_json`` recovers the JSON files.
     Heatmaps and the summary correlations come from the device in one call
     each."""
     if layout not in ("files", "columnar"):
         raise ValueError(f"layout must be 'files' or 'columnar', got {layout!r}")
     started = time.time()
+    clock = {}
+    t0 = time.perf_counter()
     out_dir = Path(out_dir)
     out_dir.mkdir(parents=True, exist_ok=True)
     pairs = [(s, k) for s in series_list for k in config.models]
     rows = train_many(pairs, config, br_hidden_of=br_hidden_of).results
+    clock["train_predict_metrics_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
     rows.sort(key=lambda r: (r.key, r.kind))
     if rows and all(r.error is not None for r in rows):
         raise RuntimeError("all series failed; first error: " + str(rows[0].error))
+    last = [time.perf_counter()]
+
+    def mark(name):  # per-stage wall clock into ExperimentOutput.timing
+        now = time.perf_counter()
+        clock[name] = now - last[0]
+        last[0] = now
+
     summaries = summarize(rows, config.split_mode)
+    mark("summarize_s")
     write_report_csv(rows, out_dir / "report.csv")
     write_summary_csv(summaries, config.split_mode, out_dir / "summary.csv")
-    write_split_manifests(series_list, config.split_spec(), out_dir)
+    if layout == "files":
+        write_split_manifests(series_list, config.split_spec(), out_dir)
+    else:
+        write_splits_columnar(series_list, config.split_spec(), out_dir / "splits.npz")
+    mark("report_summary_splits_s")
     hm_idx, hm_edges, hm_counts = device_heatmaps(rows, config.heatmap_bins)
+    mark("heatmaps_s")
     kdes = []
-    for s in series_list:
-        try:
-            kdes.append((s.key, metrics.kde(s.y)))
-        except (metrics.BandwidthError, metrics.MetricShapeError):
-            continue
+    if layout == "files":  # host numpy: the reference's kde_*.csv byte for byte
+        for s in series_list:
+            try:
+                kdes.append((s.key, metrics.kde(s.y)))
+            except (metrics.BandwidthError, metrics.MetricShapeError):
+                continue
+    else:  # one device call for every series (bbml_kde; within 1e-12 of numpy)
+        grid, dens, bw = engine.kde([s.y for s in series_list])
+        kdes = [(s.key, metrics.KdeCurve(grid[i], dens[i], float(bw[i])))
+                for i, s in enumerate(series_list) if bw[i] > 0.0]
+    mark("kde_s")
     if layout == "files":
         models_dir = out_dir / "models"
         models_dir.mkdir(exist_ok=True)
@@ -687,13 +784,20 @@ def run_experiment(series_list: Sequence[BbSeries], config: ExperimentConfig,
             write_kde_csv(curve, out_dir / f"kde_{series_slug(key)}.csv")
     else:
         write_models_columnar(rows, out_dir / "models.npz")
+        mark("models_npz_s")
+        flat = hm_counts.reshape(len(hm_idx), -1)  # sparse: most bins are empty
+        mi, bi = np.nonzero(flat)
         np.savez(out_dir / "heatmaps.npz",
                  slug=np.array([series_slug(rows[i].key, rows[i].kind) for i in hm_idx]).astype(str),
-                 edges=hm_edges, counts=hm_counts)
+                 edges=hm_edges, bins=np.array(config.heatmap_bins), model=mi.astype(np.int32),
+                 bin=bi.astype(np.int32), count=flat[mi, bi].astype(np.int32))
+        # the grid is linspace(lo, hi, 256): stored as its two ends
         np.savez(out_dir / "kde.npz", slug=np.array([series_slug(k) for k, _ in kdes]).astype(str),
-                 grid=np.stack([c.grid for _, c in kdes]) if kdes else np.zeros((0, 256)),
+                 lo=np.array([c.grid[0] for _, c in kdes]), hi=np.array([c.grid[-1] for _, c in kdes]),
                  density=np.stack([c.density for _, c in kdes]) if kdes else np.zeros((0, 256)),
                  bandwidth=np.array([c.bandwidth for _, c in kdes]))
+        mark("heatmaps_kde_npz_s")
+    clock["artifacts_s"] = time.perf_counter() - t0
     manifest = {
         "config": config.to_manifest(),
         "inputs": input_digests or {},
@@ -706,4 +810,6 @@ def run_experiment(series_list: Sequence[BbSeries], config: ExperimentConfig,
     with open(out_dir / "manifest.json", "w", encoding="utf-8", newline="\n") as fh:
         json.dump(manifest, fh, indent=2)
         fh.write("\n")
-    return ExperimentOutput(rows, summaries, out_dir)
+    out = ExperimentOutput(rows, summaries, out_dir)
+    out.timing = clock  # not in the manifest: it would break byte-identical reruns
+    return out

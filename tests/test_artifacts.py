@@ -11,8 +11,10 @@ reference: acceptance criterion 8's configuration plus three more apps).
 * heatmaps / model JSON: same structure, values within the same tolerance,
   integer counts equal where the bin edges agree;
 * summary.csv is byte-identical across two runs (criterion 8 itself);
-* the columnar layout (models.npz / heatmaps.npz / kde.npz) exports exactly
-  the per-file layout's bytes.
+* the columnar layout (models.npz / heatmaps.npz / kde.npz / splits.npz)
+  exports exactly the per-file layout's model JSON and heatmap bytes; its
+  device KDE curves agree with the host numpy ones to 1e-11 and its split
+  codes with the CSV labels.
 """
 
 import csv
@@ -106,11 +108,25 @@ def test_columnar_layout_exports_the_file_layout(golden, tmp_path):
     assert n == len(list((f / "models").glob("*.json")))
     for p in (f / "models").glob("*.json"):
         assert (c / "models_export" / p.name).read_bytes() == p.read_bytes(), p.name
-    hm = np.load(c / "heatmaps.npz")
-    for slug, edges, counts in zip(hm["slug"], hm["edges"], hm["counts"]):
-        E.write_heatmap_csv(E.metrics.HeatmapData(edges, counts), c / "x.csv")
+    hms = E.read_heatmaps_columnar(c / "heatmaps.npz")
+    assert len(hms) == len(list(f.glob("heatmap_*.csv")))
+    for slug, data in hms.items():
+        E.write_heatmap_csv(data, c / "x.csv")
         assert (c / "x.csv").read_bytes() == (f / f"heatmap_{slug}.csv").read_bytes(), slug
-    kd = np.load(c / "kde.npz")
-    for slug, grid, dens, bw in zip(kd["slug"], kd["grid"], kd["density"], kd["bandwidth"]):
-        E.write_kde_csv(E.metrics.KdeCurve(grid, dens, float(bw)), c / "k.csv")
-        assert (c / "k.csv").read_bytes() == (f / f"kde_{slug}.csv").read_bytes(), slug
+    kd = E.read_kde_columnar(c / "kde.npz")  # device KDE (bbml_kde) vs the host numpy curves
+    assert sorted(kd) == sorted(p.name[4:-4] for p in f.glob("kde_*.csv"))
+    for slug, curve in kd.items():
+        want = np.loadtxt(f / f"kde_{slug}.csv", delimiter=",", skiprows=1)
+        np.testing.assert_allclose(curve.grid, want[:, 0], rtol=1e-12, atol=0)
+        np.testing.assert_allclose(curve.density, want[:, 1], rtol=1e-11, atol=1e-300)
+    sp = np.load(c / "splits.npz")  # per-row partitions == the splits_<app>.csv labels
+    labels = {}
+    for p in f.glob("splits_*.csv"):
+        for line in p.read_text().splitlines()[1:]:
+            parts = line.split(",")
+            labels.setdefault((parts[0], int(parts[1]), int(parts[2])), []).append(parts[-1])
+    names = {-1: "error", 0: "discarded", 1: "train", 2: "test"}
+    for i, key in enumerate(zip(sp["app"], sp["kernel_id"], sp["bb_id"])):
+        key = (str(key[0]), int(key[1]), int(key[2]))
+        got = [names[int(v)] for v in sp["partition"][sp["offsets"][i]:sp["offsets"][i + 1]]]
+        assert got == labels[key], key
