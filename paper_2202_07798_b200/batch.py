@@ -338,11 +338,13 @@ class DeviceWorkload:
 
 
 def _launches_pnn(tab) -> int:
+    """Kernels bbml_pnn_train launches: one row-conversion pass (FP64 TMA
+    records / FP32 rows) plus one trainer per (d, hidden) bucket."""
     if not len(tab):
         return 0
     dm = np.where(tab["d"] <= 2, 2, np.where(tab["d"] <= 4, 4, 16))
     hm = np.where(tab["h"] <= 16, 16, 64)
-    return len(set(zip(dm.tolist(), hm.tolist())))
+    return 1 + len(set(zip(dm.tolist(), hm.tolist())))
 
 
 def _launches_lm(tab) -> int:
