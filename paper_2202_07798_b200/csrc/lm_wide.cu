@@ -37,7 +37,7 @@ __device__ unsigned long long g_wide_prof[8];
 #define WP_ADD(k, t0) (void)0
 #endif
 
-constexpr int WNT = 256;
+constexpr int WNT = 512;
 constexpr int WWARPS = WNT / 32;
 constexpr int WPMAX = 512;
 
@@ -55,6 +55,7 @@ struct WideLaunch {
   int64_t slab_doubles;   // doubles per slab
   int32_t ld;             // leading dimension of the P x P matrices (>= P, multiple of 4)
   int* queue;             // next-task counter of the persistent grid
+  int32_t dyn_doubles;    // dynamic shared memory per CTA (doubles)
 };
 
 struct WideSmem {
@@ -142,7 +143,7 @@ __device__ __host__ __forceinline__ int wide_rw(int P) {
 // of up to WCAP consecutive tiles of the row-major upper-triangle list (so
 // the A fragment is reused along the run); accumulators stay in registers
 // across all chunks.
-constexpr int WCAP = 36;
+constexpr int WCAP = 18;
 
 // Packed J'J: the strict upper triangle lives in the upper half of the P x P
 // slab (row a < column b) and the diagonal in ld doubles after it; the lower
@@ -563,108 +564,165 @@ __device__ bool wide_solve(double* A, const double* jtj, int ld, int P, double a
 // per-lane column partials reduced across warps), so each element is read
 // and written once per step instead of read twice and written once, and only
 // the lower triangle is touched.  Leaves diag / off-diag in S.dd / S.ee.
-constexpr int WCOLS = WPMAX / 32;  // column partials per lane
+// Where the trailing triangle lives: the slab's lower triangle in global
+// memory (row i at A + i*ld) while it is larger than the shared-memory
+// budget, then (from step ks on) packed in shared memory, row i >= ks holding
+// columns ks..i at T + tri(i - ks).  A step reads every trailing element once,
+// so the global phase is bound by the L2 round trip per row and the
+// shared-memory phase by issue; at P = 257 the triangle fits after ~50 steps.
+struct TriGlobal {
+  double* A;
+  int ld;
+  __device__ __forceinline__ double* row(int i) const { return A + (int64_t)i * ld; }
+};
+struct TriShared {
+  double* T;
+  int ks;
+  __device__ __forceinline__ double* row(int i) const {
+    const int m = i - ks;
+    return T + (m * (m + 1) / 2 - ks);
+  }
+};
 
-__device__ void wide_tridiag(double* A, const double* jtj, int ld, int P, WideSmem& S, double* dyn) {
+__device__ __forceinline__ int tri_count(int m) { return m * (m + 1) / 2; }
+
+// step k of the reduction (column k brought up to date and reflected, then
+// the fused sweep over rows/cols > k); WC column partials per lane (32 WC >= P)
+template <int WC, class Rows>
+__device__ __forceinline__ void tri_step(int k, int P, bool& pend, const Rows& R, WideSmem& S,
+                                         double* colp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* vp = S.v;    // pending reflector (step k-1)
   double* wp = S.pv;   // pending rank-2 partner
   double* vn = S.e2;   // reflector of step k (e2 is free until the Sturm stage)
   double* rowp = S.wt; // row dot products (wt is free during the evidence update)
-  double* colp = dyn;  // WWARPS x P column partials
-  for (int a = warp; a < P; a += WWARPS)
-    for (int b = lane; b <= a; b += 32) A[(int64_t)a * ld + b] = jtj_at(jtj, ld, a, b);
+  double part = 0.0;
+  for (int i = k + threadIdx.x; i < P; i += WNT) {
+    double* a = R.row(i) + k;
+    double x = *a;
+    if (pend) {
+      x -= fma(vp[i], wp[k], wp[i] * vp[k]);
+      *a = x;
+    }
+    if (i > k) part = fma(x, x, part);
+  }
+  const double sig = bsum(part, S);
+  const double x0 = R.row(k + 1)[k];
+  const double akk = R.row(k)[k];
+  const bool refl = sig - x0 * x0 > 0.0;
+  const double al = x0 > 0.0 ? -sqrt(sig) : sqrt(sig);
+  const double bh = refl ? 1.0 / (sig - al * x0) : 0.0;
+  for (int i = k + 1 + threadIdx.x; i < P; i += WNT)
+    vn[i] = refl ? R.row(i)[k] - (i == k + 1 ? al : 0.0) : 0.0;
+  if (threadIdx.x == 0) {
+    S.dd[k] = akk;
+    S.ee[k] = refl ? al : x0;
+  }
+  __syncthreads();
+  double cacc[WC];
+#pragma unroll
+  for (int t = 0; t < WC; ++t) cacc[t] = 0.0;
+  for (int i = k + 1 + warp; i < P; i += WWARPS) {
+    double* ai = R.row(i);
+    const double vpi = pend ? vp[i] : 0.0, wpi = pend ? wp[i] : 0.0, vni = vn[i];
+    double racc = 0.0, av[WC];
+#pragma unroll
+    for (int t = 0; t < WC; ++t) {  // all loads of the row segment in flight first
+      const int j = k + 1 + lane + 32 * t;
+      av[t] = j <= i ? ai[j] : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < WC; ++t) {
+      const int j = k + 1 + lane + 32 * t;
+      if (j <= i) {
+        double a = av[t];
+        if (pend) {
+          a -= fma(vpi, wp[j], wpi * vp[j]);
+          ai[j] = a;
+        }
+        racc = fma(a, vn[j], racc);
+        if (j < i) cacc[t] = fma(a, vni, cacc[t]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, o);
+    if (lane == 0) rowp[i] = racc;
+  }
+#pragma unroll
+  for (int t = 0; t < WC; ++t) {
+    const int j = k + 1 + lane + 32 * t;
+    if (j < P) colp[warp * P + j] = cacc[t];
+  }
+  __syncthreads();
+  double kp = 0.0;
+  for (int i = k + 1 + threadIdx.x; i < P; i += WNT) {
+    double pi = rowp[i];
+#pragma unroll
+    for (int w = 0; w < WWARPS; ++w) pi += colp[w * P + i];
+    pi *= bh;
+    rowp[i] = pi;
+    kp = fma(vn[i], pi, kp);
+  }
+  const double K = 0.5 * bh * bsum(kp, S);
+  for (int i = k + 1 + threadIdx.x; i < P; i += WNT) {
+    wp[i] = rowp[i] - K * vn[i];
+    vp[i] = vn[i];
+  }
+  if (threadIdx.x == 0) {  // entries <= k of the new pending vectors are unused
+    vp[k] = 0.0;
+    wp[k] = 0.0;
+  }
+  pend = refl;
+  __syncthreads();
+}
+
+// Householder reduction of J'J to tridiagonal form (the eigenvalue problem of
+// brbpnn.py:221-236), one block-wide step per column.  The whole CTA makes one
+// pass over the trailing lower triangle per step: the rank-2 update of step
+// k-1 (A -= v w' + w v') is applied in the same sweep that forms p = A v of
+// step k (row dot products by warp reductions, the transposed half by
+// per-lane column partials reduced across warps), so each element is read
+// and written once per step instead of read twice and written once, and only
+// the lower triangle is touched.  dyn holds the WWARPS x P column partials
+// and, after them, the shared-memory copy of the trailing triangle
+// (dyn_doubles in all).  Leaves diag / off-diag in S.dd / S.ee.
+template <int WC>
+__device__ void wide_tridiag(double* A, const double* jtj, int ld, int P, WideSmem& S, double* dyn,
+                             int dyn_doubles) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* colp = dyn;
+  double* T = dyn + ((WWARPS * P + 1) & ~1);
+  const int cap = dyn_doubles - ((WWARPS * P + 1) & ~1);
+  int ks = 0;
+  while (ks + 2 < P && tri_count(P - ks) > cap) ++ks;
+  const TriGlobal G{A, ld};
+  const TriShared SH{T, ks};
+  if (ks == 0) {
+    for (int a = warp; a < P; a += WWARPS)
+      for (int b = lane; b <= a; b += 32) SH.row(a)[b] = jtj_at(jtj, ld, a, b);
+  } else {
+    for (int a = warp; a < P; a += WWARPS)
+      for (int b = lane; b <= a; b += 32) G.row(a)[b] = jtj_at(jtj, ld, a, b);
+  }
   bool pend = false;
   __syncthreads();
-  for (int k = 0; k + 2 < P; ++k) {
-    // column k (rows >= k) brought up to date with the pending update
-    double part = 0.0;
-    for (int i = k + threadIdx.x; i < P; i += WNT) {
-      double* a = A + (int64_t)i * ld + k;
-      double x = *a;
-      if (pend) {
-        x -= fma(vp[i], wp[k], wp[i] * vp[k]);
-        *a = x;
-      }
-      if (i > k) part = fma(x, x, part);
-    }
-    const double sig = bsum(part, S);
-    const double x0 = A[(int64_t)(k + 1) * ld + k];
-    const double akk = A[(int64_t)k * ld + k];
-    const bool refl = sig - x0 * x0 > 0.0;
-    const double al = x0 > 0.0 ? -sqrt(sig) : sqrt(sig);
-    const double bh = refl ? 1.0 / (sig - al * x0) : 0.0;
-    for (int i = k + 1 + threadIdx.x; i < P; i += WNT)
-      vn[i] = refl ? A[(int64_t)i * ld + k] - (i == k + 1 ? al : 0.0) : 0.0;
-    if (threadIdx.x == 0) {
-      S.dd[k] = akk;
-      S.ee[k] = refl ? al : x0;
-    }
-    __syncthreads();
-    // fused sweep over the trailing lower triangle (rows/cols > k)
-    double cacc[WCOLS];
-#pragma unroll
-    for (int t = 0; t < WCOLS; ++t) cacc[t] = 0.0;
-    for (int i = k + 1 + warp; i < P; i += WWARPS) {
-      double* ai = A + (int64_t)i * ld;
-      const double vpi = pend ? vp[i] : 0.0, wpi = pend ? wp[i] : 0.0, vni = vn[i];
-      double racc = 0.0, av[WCOLS];
-#pragma unroll
-      for (int t = 0; t < WCOLS; ++t) {  // all loads of the row segment in flight first
-        const int j = k + 1 + lane + 32 * t;
-        av[t] = j <= i ? ai[j] : 0.0;
-      }
-#pragma unroll
-      for (int t = 0; t < WCOLS; ++t) {
-        const int j = k + 1 + lane + 32 * t;
-        if (j <= i) {
-          double a = av[t];
-          if (pend) {
-            a -= fma(vpi, wp[j], wpi * vp[j]);
-            ai[j] = a;
-          }
-          racc = fma(a, vn[j], racc);
-          if (j < i) cacc[t] = fma(a, vni, cacc[t]);
-        }
-      }
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, o);
-      if (lane == 0) rowp[i] = racc;
-    }
-#pragma unroll
-    for (int t = 0; t < WCOLS; ++t) {
-      const int j = k + 1 + lane + 32 * t;
-      if (j < P) colp[warp * P + j] = cacc[t];
-    }
-    __syncthreads();
-    double kp = 0.0;
-    for (int i = k + 1 + threadIdx.x; i < P; i += WNT) {
-      double pi = rowp[i];
-#pragma unroll
-      for (int w = 0; w < WWARPS; ++w) pi += colp[w * P + i];
-      pi *= bh;
-      rowp[i] = pi;
-      kp = fma(vn[i], pi, kp);
-    }
-    const double K = 0.5 * bh * bsum(kp, S);
-    for (int i = k + 1 + threadIdx.x; i < P; i += WNT) {
-      wp[i] = rowp[i] - K * vn[i];
-      vp[i] = vn[i];
-    }
-    if (threadIdx.x == 0) {  // entries <= k of the new pending vectors are unused
-      vp[k] = 0.0;
-      wp[k] = 0.0;
-    }
-    pend = refl;
+  int k = 0;
+  WP_T(tg);
+  for (; k < ks && k + 2 < P; ++k) tri_step<WC>(k, P, pend, G, S, colp);
+  WP_ADD(5, tg);
+  if (ks > 0 && ks + 2 < P) {  // trailing rows/cols >= ks into shared memory
+    for (int a = ks + warp; a < P; a += WWARPS)
+      for (int b = ks + lane; b <= a; b += 32) SH.row(a)[b] = G.row(a)[b];
     __syncthreads();
   }
+  const bool sh = ks + 2 < P || ks == 0;
+  for (; k + 2 < P; ++k) tri_step<WC>(k, P, pend, SH, S, colp);
   // last 2x2 block
   if (threadIdx.x < 3) {
-    const int i = P - 2 + (threadIdx.x > 0), j = P - 2 + (threadIdx.x > 1);
-    double* a = A + (int64_t)(threadIdx.x == 1 ? P - 1 : i) * ld + (threadIdx.x == 1 ? P - 2 : j);
-    const int ii = threadIdx.x == 1 ? P - 1 : i, jj = threadIdx.x == 1 ? P - 2 : j;
-    double x = *a;
-    if (pend) x -= fma(vp[ii], wp[jj], wp[ii] * vp[jj]);
+    const int i = threadIdx.x == 1 ? P - 1 : P - 2 + (threadIdx.x > 0);
+    const int j = threadIdx.x == 1 ? P - 2 : P - 2 + (threadIdx.x > 1);
+    double x = sh ? SH.row(i)[j] : G.row(i)[j];
+    if (pend) x -= fma(S.v[i], S.pv[j], S.pv[i] * S.v[j]);
     if (threadIdx.x == 0) S.dd[P - 2] = x;
     else if (threadIdx.x == 1) S.ee[P - 2] = x;
     else S.dd[P - 1] = x;
@@ -673,8 +731,9 @@ __device__ void wide_tridiag(double* A, const double* jtj, int ld, int P, WideSm
 }
 
 __device__ double wide_gamma(double* A, const double* jtj, int ld, int P, double alpha, double beta,
-                             WideSmem& S, double* dyn) {
-  wide_tridiag(A, jtj, ld, P, S, dyn);
+                             WideSmem& S, double* dyn, int dyn_doubles) {
+  if (P <= 9 * 32) wide_tridiag<9>(A, jtj, ld, P, S, dyn, dyn_doubles);
+  else wide_tridiag<WPMAX / 32>(A, jtj, ld, P, S, dyn, dyn_doubles);
   WP_T(tb);
   double glo = 1e308, ghi = -1e308;
   for (int i = threadIdx.x; i < P; i += WNT) {
@@ -803,7 +862,7 @@ __device__ __forceinline__ void lm_wide_fit(const WideLaunch& L, int task, doubl
       have_stats = true;
       jtj_ok = true;
       WP_T(t1);
-      gamma = wide_gamma(A, jtj, ld, P, alpha, beta, S, wdyn);
+      gamma = wide_gamma(A, jtj, ld, P, alpha, beta, S, wdyn, L.dyn_doubles);
       WP_ADD(1, t1);
       double na, nb;
       if (e_w > 0.0) {
@@ -911,7 +970,19 @@ bbml_status lm_wide_launch(const bbml_lm_task* d_tasks, const int32_t* d_orig,
   const int ld = (pmax + 3) & ~3;
   const int64_t slab = (int64_t)ld * ld + ld;  // packed J'J + workspace, one array
   const int rw = wide_rw(pmax);
-  const size_t dyn = (size_t)(WNB * rw + 32 * 33) * sizeof(double);
+  // dynamic shared memory: the [J r] chunk / Cholesky panel, or during the
+  // tridiagonalisation the column partials + the trailing triangle; the
+  // latter takes everything the opt-in limit leaves (one CTA per SM anyway:
+  // 512 threads x 128 registers)
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{}, fb{};
+  cudaFuncGetAttributes(&fa, lm_wide_kernel);
+  cudaFuncGetAttributes(&fb, lm_wide_kernel_once);
+  const size_t stat = std::max(fa.sharedSizeBytes, fb.sharedSizeBytes);
+  const size_t need = (size_t)(WNB * rw + 32 * 33) * sizeof(double);
+  const size_t dyn = std::max(need, ((size_t)optin > stat ? (size_t)optin - stat : 0) & ~(size_t)15);
   (void)nmax;
   static_assert(WCH == WNB, "chunk rows and panel width share the dynamic buffer");
   cudaError_t ea = cudaFuncSetAttribute(lm_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -919,8 +990,7 @@ bbml_status lm_wide_launch(const bbml_lm_task* d_tasks, const int32_t* d_orig,
   if (ea == cudaSuccess)
     ea = cudaFuncSetAttribute(lm_wide_kernel_once, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (ea != cudaSuccess) return cuda_status(ea, "lm_wide smem");
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
+  int sms = 0, per_sm = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lm_wide_kernel, WNT, dyn);
   const int grid = std::min(n_tasks, std::max(1, per_sm) * sms);
@@ -947,6 +1017,7 @@ bbml_status lm_wide_launch(const bbml_lm_task* d_tasks, const int32_t* d_orig,
   L.slab_doubles = slab;
   L.ld = ld;
   L.queue = (int*)(d_scratch + slab * grid);
+  L.dyn_doubles = (int32_t)(dyn / sizeof(double));
   if (grid == n_tasks) lm_wide_kernel_once<<<grid, WNT, dyn, s>>>(L);
   else lm_wide_kernel<<<grid, WNT, dyn, s>>>(L);
   cudaError_t e = cudaGetLastError();
@@ -955,8 +1026,8 @@ bbml_status lm_wide_launch(const bbml_lm_task* d_tasks, const int32_t* d_orig,
     unsigned long long pr[8];
     cudaStreamSynchronize(s);
     cudaMemcpyFromSymbol(pr, g_wide_prof, sizeof(pr));
-    fprintf(stderr, "[wide_prof] Mcycles stats %.1f gamma %.1f (bisect %.1f) solve %.1f energy %.1f\n",
-            pr[0] * 1e-6, pr[1] * 1e-6, pr[4] * 1e-6, pr[2] * 1e-6, pr[3] * 1e-6);
+    fprintf(stderr, "[wide_prof] Mcycles stats %.1f gamma %.1f (bisect %.1f, tridiag global phase %.1f) solve %.1f energy %.1f\n",
+            pr[0] * 1e-6, pr[1] * 1e-6, pr[4] * 1e-6, pr[5] * 1e-6, pr[2] * 1e-6, pr[3] * 1e-6);
     const unsigned long long z[8] = {};
     cudaMemcpyToSymbol(g_wide_prof, z, sizeof(z));
   }
