@@ -756,11 +756,18 @@ __device__ double wide_gamma(double* A, const double* jtj, int ld, int P, double
   }
   __syncthreads();
   const double hi0 = (ghi + 2.220446049250313e-16 * tnorm) * scale;
-  const int n_neg = sturm_count(S.dd, S.e2, P, 0.0);
+  // rows {d_j, e_{j-1}^2} padded to a multiple of 4 (d = 2 > ||T||, e = 0)
+  // in the dynamic buffer (free after the reduction)
+  const int n4 = (P + 3) & ~3;
+  double2* de = reinterpret_cast<double2*>(dyn);
+  for (int i = threadIdx.x; i < n4; i += WNT)
+    de[i] = make_double2(i < P ? S.dd[i] : 2.0, (i >= 1 && i < P) ? S.e2[i - 1] : 0.0);
+  __syncthreads();
+  const int n_tiny = sturm_count_rt(de, kFixTiny, n4);
   const double r = alpha / beta * scale;
   double part = 0.0;
   for (int idx = threadIdx.x; idx < P; idx += WNT)
-    part += sturm_gamma_part(S.dd, S.e2, P, idx, n_neg, hi0, r, 1.0 / scale, alpha, beta);
+    part += sturm_gamma_part_rt(de, n4, idx, n_tiny, hi0, r, 1.0 / scale, alpha, beta);
   const double g = bsum(part, S);
   WP_ADD(4, tb);
   return g;

@@ -9,16 +9,21 @@
 //       p_j = (d_j - x) p_{j-1} - e_{j-1}^2 p_{j-2}
 //     (q_j = p_j / p_{j-1} is the LDL' pivot of T - xI; q_j < 0 <=> sign change;
 //     |q_j| below a tiny floor is replaced by -floor, LAPACK dlaebz's pivmin rule),
-//     rescaled by powers of two to stay in range.  One dependent DFMA per row
-//     instead of a DDIV.
-//   * eigenvalues below 0 (one shared count at x = 0) contribute 0 (clipped);
-//     the others bisect [0, ||T||] on the IEEE bit pattern (the midpoint of the
-//     bit patterns is the geometric midpoint across binades, the arithmetic one
-//     inside a binade), so near-null eigenvalues converge in relative terms.
+//     renormalised by powers of two every fourth row.  One dependent DFMA
+//     per row instead of a DDIV.
+//   * eigenvalues below 2^-200 (scaled; negative ones included, one shared
+//     count) contribute 0 -- the reference's clip at 0 up to < 2^-200 / r;
+//     the others bisect [2^-200, ||T||] on the IEEE bit pattern (the midpoint
+//     of the bit patterns is the geometric midpoint across binades, the
+//     arithmetic one inside a binade), so near-null eigenvalues converge in
+//     relative terms.
 //   * stop when the gamma contribution is pinned (1e-13; 1e-10 for the P <= 32
 //     warp path) (division-free form
 //     of f(hi) - f(lo) = r (hi-lo) / ((hi+r)(lo+r)), r = alpha/beta) or at
 //     ~2 ulp relative width.
+// T rows live in shared memory as {d_j, e_{j-1}^2} pairs, padded with
+// d = 2 (> ||T||), e = 0 rows that never change sign: compile-time length
+// (warp path, P <= 32) or P rounded up to 4 (wide path).
 // Eigenvalue accuracy is the backward-stable eps*||T|| of bisection, the same
 // class as LAPACK dsyevd used by the reference.
 #pragma once
@@ -26,36 +31,12 @@
 
 namespace bbml {
 
-constexpr double kSturmPiv = 0x1p-400;  // pivot floor relative to |p_{j-1}| (scaled T)
-
 // 2^-ceil(log2(t)) for t > 0 (exact power of two), so t * scale <= 1
 __device__ __forceinline__ double sturm_scale(double t) {
   int e;
   const double m = frexp(t, &e);  // t = m * 2^e, m in [0.5, 1)
   (void)m;
   return ldexp(1.0, -e);
-}
-
-// number of eigenvalues of the scaled T below x
-__device__ __forceinline__ int sturm_count(const double* __restrict__ dd,
-                                           const double* __restrict__ e2, int P, double x) {
-  double p0 = 1.0, p1 = dd[0] - x;
-  if (fabs(p1) < kSturmPiv) p1 = -kSturmPiv;
-  int cnt = p1 < 0.0;
-#pragma unroll 4
-  for (int j = 1; j < P; ++j) {
-    const double fl = kSturmPiv * p1;
-    double p2 = fma(dd[j] - x, p1, -(e2[j - 1] * p0));
-    p2 = fabs(p2) < fabs(fl) ? -fl : p2;
-    cnt += (__double2hiint(p2) ^ __double2hiint(p1)) < 0;
-    p0 = p1;
-    p1 = p2;
-    const double m = fmax(fabs(p0), fabs(p1));
-    const double s = m > 0x1p200 ? 0x1p-400 : (m < 0x1p-200 ? 0x1p400 : 1.0);
-    p0 *= s;
-    p1 *= s;
-  }
-  return cnt;
 }
 
 // Fixed-length variant for the warp path (P <= PM <= 32): T padded to PM
@@ -135,16 +116,45 @@ __device__ __forceinline__ double sturm_gamma_part_fixed(const double2* __restri
   return den > 0.0 ? __ddiv_rn(sc, den) : 0.0;
 }
 
-// gamma contribution of the k-th smallest eigenvalue (0-based).  dd/e2 are the
-// scaled diagonal and squared off-diagonal; hi0 = scaled Gershgorin upper
-// bound; n_neg = sturm_count(0); r = (alpha/beta) * scale; inv_scale = 1/scale.
-__device__ __forceinline__ double sturm_gamma_part(const double* __restrict__ dd,
-                                                   const double* __restrict__ e2, int P, int k,
-                                                   int n_neg, double hi0, double r,
-                                                   double inv_scale, double alpha, double beta) {
-  if (k < n_neg || !(hi0 > 0.0)) return 0.0;  // eigenvalue <= 0: clipped
-  double lo = 0.0, hi = hi0;
-  long long lb = 0, hb = __double_as_longlong(hi0);
+// Runtime-length form of the fixed count for the wide path: de = {d_j,
+// e_{j-1}^2} padded to n4 (P rounded up to 4) rows with d = 2, e = 0.  Row 0
+// runs through the recurrence with p_{-1} = 1, p_{-2} = 0 (the same values as
+// the explicit first row above); renormalised every fourth row.
+__device__ __forceinline__ int sturm_count_rt(const double2* __restrict__ de, double x, int n4) {
+  double p0 = 0.0, p1 = 1.0;
+  int cnt = 0;
+  auto row = [&](int j) {
+    const double2 v = de[j];
+    const double fl = kFixPiv * p1;
+    double p2 = fma(v.x - x, p1, -(v.y * p0));
+    p2 = fabs(p2) < fabs(fl) ? -fl : p2;
+    cnt += (int)((unsigned)(__double2hiint(p2) ^ __double2hiint(p1)) >> 31);
+    p0 = p1;
+    p1 = p2;
+  };
+#pragma unroll 1
+  for (int j = 0; j < n4; j += 4) {
+    row(j);
+    row(j + 1);
+    row(j + 2);
+    row(j + 3);
+    const int hm = max(__double2hiint(p0) & 0x7fffffff, __double2hiint(p1) & 0x7fffffff);
+    const double sc = __hiloint2double((2046 - (hm >> 20)) << 20, 0);
+    p0 *= sc;
+    p1 *= sc;
+  }
+  return cnt;
+}
+
+// wide path: gamma contribution of the k-th smallest eigenvalue with the
+// runtime-length count (pin 1e-13; eigenvalues below kFixTiny clipped, as in
+// the warp path)
+__device__ __forceinline__ double sturm_gamma_part_rt(const double2* __restrict__ de, int n4, int k,
+                                                      int n_tiny, double hi0, double r,
+                                                      double inv_scale, double alpha, double beta) {
+  if (k < n_tiny || !(hi0 > kFixTiny)) return 0.0;
+  double lo = kFixTiny, hi = hi0;
+  long long lb = __double_as_longlong(lo), hb = __double_as_longlong(hi0);
   constexpr double eps = 2.220446049250313e-16;
   for (int it = 0; it < 80; ++it) {
     const double w = hi - lo;
@@ -152,7 +162,7 @@ __device__ __forceinline__ double sturm_gamma_part(const double* __restrict__ dd
     if (w * r <= 1e-13 * ((hi + r) * (lo + r))) break;
     const long long mb = (lb + hb) >> 1;
     const double mid = __longlong_as_double(mb);
-    if (sturm_count(dd, e2, P, mid) > k) {
+    if (sturm_count_rt(de, mid, n4) > k) {
       hi = mid;
       hb = mb;
     } else {
