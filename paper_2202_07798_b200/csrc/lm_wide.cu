@@ -26,7 +26,7 @@
 namespace bbml {
 
 #ifdef BBML_LM_PROF
-__device__ unsigned long long g_wide_prof[8];
+__device__ unsigned long long g_wide_prof[16];
 #define WP_T(v) long long v = clock64()
 #define WP_ADD(k, t0)                                                                     \
   do {                                                                                    \
@@ -273,6 +273,7 @@ __device__ bool wide_chol(double* A, const double* jtj, int ld, int P, double al
   const int rw = wide_rw(P);
   double* PT = dyn;               // panel, transposed: PT[t * rw + i]
   double* D = dyn + WNB * rw;     // diagonal block, 32 x 33
+  WP_T(tc0);
   for (int a = warp; a < P; a += WWARPS)
     for (int b = lane; b <= a; b += 32) {
       const double v = __dmul_rn(beta, jtj_at(jtj, ld, a, b));
@@ -281,8 +282,10 @@ __device__ bool wide_chol(double* A, const double* jtj, int ld, int P, double al
   for (int a = threadIdx.x; a < P; a += WNT)
     S.rhs[a] = -__dadd_rn(__dmul_rn(beta, S.jtr[a]), __dmul_rn(alpha, S.w[a]));
   __syncthreads();
+  WP_ADD(8, tc0);
   for (int kb = 0; kb < P; kb += WNB) {
     const int nb = min(WNB, P - kb), r0 = kb + nb, m = P - r0;
+    WP_T(tc1);
     for (int e = threadIdx.x; e < nb * nb; e += WNT) {
       const int i = e / nb, j = e - i * nb;
       D[i * 33 + j] = j <= i ? A[(int64_t)(kb + i) * ld + kb + j] : 0.0;
@@ -310,6 +313,8 @@ __device__ bool wide_chol(double* A, const double* jtj, int ld, int P, double al
       if (lane == 0) S.piv = bad ? 1 : 0;
     }
     __syncthreads();
+    WP_ADD(9, tc1);
+    WP_T(tc2);
     if (S.piv) return false;
     for (int e = threadIdx.x; e < nb * nb; e += WNT) {
       const int i = e / nb, j = e - i * nb;
@@ -339,6 +344,8 @@ __device__ bool wide_chol(double* A, const double* jtj, int ld, int P, double al
         }
     }
     __syncthreads();
+    WP_ADD(10, tc2);
+    WP_T(tc3);
     // trailing update of the lower triangle: A22 -= X X'
     const int mb = (m + 3) >> 2;
     const int nt = mb * (mb + 1) / 2;
@@ -379,7 +386,9 @@ __device__ bool wide_chol(double* A, const double* jtj, int ld, int P, double al
         }
     }
     __syncthreads();
+    WP_ADD(11, tc3);
   }
+  WP_T(tc4);
   auto load_diag = [&](int kb, int nb) {  // factored diagonal block -> D (shared)
     for (int e = threadIdx.x; e < nb * nb; e += WNT) {
       const int i = e / nb, j = e - i * nb;
@@ -440,6 +449,7 @@ __device__ bool wide_chol(double* A, const double* jtj, int ld, int P, double al
     }
     __syncthreads();
   }
+  WP_ADD(12, tc4);
   return true;
 }
 
@@ -814,6 +824,9 @@ __device__ __forceinline__ void lm_wide_fit(const WideLaunch& L, int task, doubl
       WP_T(t0);
       wide_stats_dmma(jtj, ld, X, Y, n, d, h, P, xs, S, wdyn);
       WP_ADD(0, t0);
+#ifdef BBML_LM_PROF
+      if (threadIdx.x == 0) atomicAdd(&g_wide_prof[6], 1ull);
+#endif
       jtj_ok = true;
     }
     const double f0 = __dadd_rn(__dmul_rn(beta, e_d), __dmul_rn(alpha, e_w));
@@ -866,6 +879,9 @@ __device__ __forceinline__ void lm_wide_fit(const WideLaunch& L, int task, doubl
       WP_T(t0);
       wide_stats_dmma(jtj, ld, X, Y, n, d, h, P, xs, S, wdyn);
       WP_ADD(0, t0);
+#ifdef BBML_LM_PROF
+      if (threadIdx.x == 0) atomicAdd(&g_wide_prof[6], 1ull);
+#endif
       have_stats = true;
       jtj_ok = true;
       WP_T(t1);
@@ -1030,12 +1046,14 @@ bbml_status lm_wide_launch(const bbml_lm_task* d_tasks, const int32_t* d_orig,
   cudaError_t e = cudaGetLastError();
 #ifdef BBML_LM_PROF
   {
-    unsigned long long pr[8];
+    unsigned long long pr[16];
     cudaStreamSynchronize(s);
     cudaMemcpyFromSymbol(pr, g_wide_prof, sizeof(pr));
+    fprintf(stderr, "[wide_prof] stats calls %llu; chol Mcycles fill %.1f diag %.1f panel %.1f trailing %.1f subst %.1f\n", pr[6],
+            pr[8] * 1e-6, pr[9] * 1e-6, pr[10] * 1e-6, pr[11] * 1e-6, pr[12] * 1e-6);
     fprintf(stderr, "[wide_prof] Mcycles stats %.1f gamma %.1f (bisect %.1f, tridiag global phase %.1f) solve %.1f energy %.1f\n",
             pr[0] * 1e-6, pr[1] * 1e-6, pr[4] * 1e-6, pr[5] * 1e-6, pr[2] * 1e-6, pr[3] * 1e-6);
-    const unsigned long long z[8] = {};
+    const unsigned long long z[16] = {};
     cudaMemcpyToSymbol(g_wide_prof, z, sizeof(z));
   }
 #endif
