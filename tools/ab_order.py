@@ -7,7 +7,7 @@ from paper_2202_07798_b200 import batch
 import bench
 
 series, spec, kw = bench.workload_series("suite16")
-wl = batch.build_workload(series, spec, restarts=list(range(32)), precision=32, **kw)
+wl = batch.build_workload(series, spec, restarts=list(range(32)), precision=int(os.environ.get("PREC", "32")), **kw)
 dev = batch.DeviceWorkload(wl)
 s = torch.cuda.current_stream()
 for rep in range(2):
