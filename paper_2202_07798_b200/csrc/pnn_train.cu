@@ -23,6 +23,7 @@
 //                    double buffer while the consumer trains on epoch e, so the
 //                    sequential shuffle is off the training critical path.
 //   Hand-off: per-model produced/consumed epoch counters in shared memory.
+#include <cstdio>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -994,6 +995,21 @@ __host__ __device__ constexpr int f64_stage_doubles(int rec) {
   return 2 * 2 * SP * rec + 2;
 }
 
+// Development-only phase clocks of the FP64 consumer loop (compile with
+// -DBBML_PNN_PROF): lane 0 of every consumer warp accumulates clock64() per
+// phase; printed to stderr after each bbml_pnn_train call.
+#ifdef BBML_PNN_PROF
+__device__ unsigned long long g_pnn_prof[8];
+#define PP_T(v) long long v = clock64()
+#define PP_ADD(k, t0)                                                                  \
+  do {                                                                                 \
+    if (lane == 0) atomicAdd(&g_pnn_prof[k], (unsigned long long)(clock64() - (t0))); \
+  } while (0)
+#else
+#define PP_T(v) (void)0
+#define PP_ADD(k, t0) (void)0
+#endif
+
 template <int DM, int SP, typename PermT>
 __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
   const int RW = L.rec;       // staged row record: x[0..W), y at W = L.rec_y, pad
@@ -1104,9 +1120,11 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
     gb2 = bloss = 0.0;
   };
   for (int ep = 0; ep < tk.epochs; ++ep) {
+    PP_T(tp);
     while (ld_volatile(produced + gi) <= ep) {
     }
     __threadfence_block();
+    PP_ADD(5, tp);
     const PermT* perm = pbase + (ep & 1) * cap;
     double eloss = 0.0;
     zero_grads();
@@ -1129,7 +1147,10 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
         issue(buf ^ 1, perm, nbs + ns0, min(C, min(B, n - nbs) - ns0));
       }
       (void)cur_inflight;
+      PP_T(t0);
       wait(buf);
+      PP_ADD(0, t0);
+      PP_T(t1);
       const double* rows = stage + (buf * 2 + sg) * SP * RW;
 
       // forward (own unit, own half's samples)
@@ -1146,6 +1167,8 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
       for (int mm = 1; mm < 16; mm <<= 1)
 #pragma unroll
         for (int i = 0; i < SP; ++i) z[i] += __shfl_xor_sync(FULL, z[i], mm);
+      PP_ADD(1, t1);
+      PP_T(t2);
       // loss chain of sample (sg, j) on lane j < SP (pnn.py:131-138)
       double zj = z[0];
 #pragma unroll
@@ -1162,6 +1185,8 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
       const double drate = div_rn_bf(__dsub_rn(1.0, div_rn_bf(yj, re)), nb_t);
       const double dzj = mine ? __dmul_rn(drate, exp_neg_bf(__dsub_rn(zz, sp))) : 0.0;
       if (mine) bloss += __dsub_rn(rate, __dmul_rn(yj, log_bf(re)));
+      PP_ADD(2, t2);
+      PP_T(t3);
       // backward (pnn.py:139-146)
 #pragma unroll
       for (int i = 0; i < SP; ++i) {
@@ -1174,6 +1199,8 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
         for (int k = 0; k < DM; ++k) g[k] += dp * rows[i * RW + k];
       }
       __syncwarp();  // every lane has read this staging buffer
+      PP_ADD(3, t3);
+      PP_T(t4);
       buf ^= 1;
       if (ns0 == 0) {  // end of minibatch: checks + Adam (pnn.py:243-247, 174-189)
         // gradient halves: lane sg owns parameters q with q % 2 == sg; one
@@ -1203,6 +1230,8 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
         const unsigned bits = (!isfinite(bloss) ? 1u : 0u) | (bw1 ? 2u : 0u) | (bb1 ? 4u : 0u) |
                               (bw2 ? 8u : 0u) | (!isfinite(gb2) ? 16u : 0u);
         const unsigned any = __reduce_or_sync(FULL, bits);
+        PP_ADD(6, t4);
+        PP_T(t6);
         if (any) {
           double lsum = bloss;
 #pragma unroll
@@ -1231,35 +1260,42 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
         const bool b2_lane = b2_slot && sg == 0 && j == h;
         auto adam_all = [&](auto bc_tag) {
           constexpr bool BC = decltype(bc_tag)::value;
+          // all NP/2 updates first, then the commits as selects: lane-divergent
+          // stores (sg, real, b2_lane) as branches would split the updates
+          // into separate blocks and serialise their latency chains
+          double np_[NP / 2], nm_[NP / 2], nv_[NP / 2];
 #pragma unroll
           for (int i = 0; i < NP / 2; ++i) {
-            const int q = 2 * i + sg;
-            const bool real = j < h && (q >= DM || q < d);
+            const bool b2i = i == 0 && b2_lane;
             double pv = sg ? p[2 * i + 1] : p[2 * i];
             double mv = sg ? m1[2 * i + 1] : m1[2 * i];
             double vv = sg ? m2[2 * i + 1] : m2[2 * i];
             double gv = sg ? g[2 * i + 1] : g[2 * i];
-            if (i == 0 && b2_lane) {
-              pv = b2;
-              mv = mb2;
-              vv = vb2;
-              gv = gb2;
-            }
+            pv = b2i ? b2 : pv;
+            mv = b2i ? mb2 : mv;
+            vv = b2i ? vb2 : vv;
+            gv = b2i ? gb2 : gv;
             adam_exact<BC>(pv, mv, vv, gv, bc1, bc2, lr);
-            if (i == 0 && b2_lane) {
-              b2 = pv;
-              mb2 = mv;
-              vb2 = vv;
-            } else if (real) {
-              if (sg) {
-                p[2 * i + 1] = pv;
-                m1[2 * i + 1] = mv;
-                m2[2 * i + 1] = vv;
-              } else {
-                p[2 * i] = pv;
-                m1[2 * i] = mv;
-                m2[2 * i] = vv;
-              }
+            np_[i] = pv;
+            nm_[i] = mv;
+            nv_[i] = vv;
+          }
+#pragma unroll
+          for (int i = 0; i < NP / 2; ++i) {
+            const bool b2i = i == 0 && b2_lane;
+            const int q = 2 * i + sg;
+            const bool real = j < h && (q >= DM || q < d) && !b2i;
+            const bool lo = real && !sg, hi = real && sg;
+            p[2 * i] = lo ? np_[i] : p[2 * i];
+            m1[2 * i] = lo ? nm_[i] : m1[2 * i];
+            m2[2 * i] = lo ? nv_[i] : m2[2 * i];
+            p[2 * i + 1] = hi ? np_[i] : p[2 * i + 1];
+            m1[2 * i + 1] = hi ? nm_[i] : m1[2 * i + 1];
+            m2[2 * i + 1] = hi ? nv_[i] : m2[2 * i + 1];
+            if (i == 0) {
+              b2 = b2i ? np_[0] : b2;
+              mb2 = b2i ? nm_[0] : mb2;
+              vb2 = b2i ? nv_[0] : vb2;
             }
           }
           if (b2_slot) b2 = __shfl_sync(FULL, b2, h);
@@ -1267,6 +1303,7 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
         };
         if (bc1 != 1.0 || bc2 != 1.0) adam_all(std::true_type{});  // warp-uniform (t is per model)
         else adam_all(std::false_type{});
+        PP_ADD(7, t6);
         // updated weights back to the partner half
 #pragma unroll
         for (int q = 0; q + 1 < NP; q += 2) {
@@ -1278,6 +1315,7 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
         eloss += div_rn_bf(bloss, nb_t);  // this lane's share of the batch mean
         zero_grads();
       }
+      PP_ADD(4, t4);
       if (!more) break;
       bs = nbs;
       s0 = ns0;
@@ -1711,6 +1749,17 @@ bbml_status pnn_train_launch(const bbml_pnn_task* tasks, int32_t n_tasks, const 
     if (e != cudaSuccess) return cuda_status(e, "pnn_train launch");
   }
   if ((st = fork.join()) != BBML_OK) return st;
+#ifdef BBML_PNN_PROF
+  {
+    unsigned long long pr[8];
+    cudaStreamSynchronize(stream);
+    cudaMemcpyFromSymbol(pr, g_pnn_prof, sizeof(pr));
+    fprintf(stderr, "[pnn_prof] Mcycles tma-wait %.1f forward %.1f loss %.1f backward %.1f batch-end %.1f (grads+checks %.1f, adam %.1f) epoch-wait %.1f\n",
+            pr[0] * 1e-6, pr[1] * 1e-6, pr[2] * 1e-6, pr[3] * 1e-6, pr[4] * 1e-6, pr[6] * 1e-6, pr[7] * 1e-6, pr[5] * 1e-6);
+    const unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_pnn_prof, z, sizeof(z));
+  }
+#endif
   return scratch.release();
 }
 
