@@ -1179,11 +1179,16 @@ __device__ __forceinline__ void pnn_f64_body(const PnnLaunch& L) {
       const double nb_t = (double)nb;
       const double zz = __dadd_rn(zj, b2);
       // softplus = numpy logaddexp(0, z) = max(z, 0) + log1p(exp(-|z|))
-      const double sp = __dadd_rn(fmax(zz, 0.0), log1p_bf(exp_neg_bf(-fabs(zz))));
+      const double ez = exp_neg_bf(-fabs(zz));
+      const double sp = __dadd_rn(fmax(zz, 0.0), log1p_bf(ez));
       const double rate = __dadd_rn(sp, eps);
       const double re = __dadd_rn(rate, eps);
       const double drate = div_rn_bf(__dsub_rn(1.0, div_rn_bf(yj, re)), nb_t);
-      const double dzj = mine ? __dmul_rn(drate, exp_neg_bf(__dsub_rn(zz, sp))) : 0.0;
+      // d softplus / dz = sigmoid(z): the reference's exp(z - softplus(z))
+      // (pnn.py:138) evaluated as 1/(1+e) or e/(1+e) from the e = exp(-|z|)
+      // above (<= 1.5 ulp apart), off the log1p -> division chain
+      const double sg1 = div_rn_bf(zz >= 0.0 ? 1.0 : ez, __dadd_rn(1.0, ez));
+      const double dzj = mine ? __dmul_rn(drate, sg1) : 0.0;
       if (mine) bloss += __dsub_rn(rate, __dmul_rn(yj, log_bf(re)));
       PP_ADD(2, t2);
       PP_T(t3);
