@@ -2,6 +2,7 @@
 set -x
 O=gpurun_out/final; mkdir -p $O; rm -rf $O/*
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest.log 2>&1; echo pytest=$?
+timeout 900 python -m pytest tests/test_bench_parity.py -m gpu -q -s > $O/bench_parity.log 2>&1; echo bench_parity=$?
 timeout 1200 python bench.py --steps 20 --warmup 5 > $O/bench_suite16.log 2> $O/bench_suite16.err; echo suite16=$?
 timeout 1200 python bench.py --impl reference --steps 20 --warmup 5 > $O/ref_suite16.log 2> $O/ref_suite16.err; echo ref=$?
 timeout 900 python bench.py --precision 32 --no-cpu-baseline > $O/bench_suite16_fp32.log 2> $O/bench_suite16_fp32.err; echo fp32=$?
@@ -15,3 +16,4 @@ cap() { name=$1; shift; timeout 900 ncu --set full --clock-control none --import
 cap pnn_f64_long -k regex:pnn_f64_kernel -o $O/pnn_f64_long python tools/prof.py --precision 64 --kind pnn --app pathfinder --epochs 10 --reps 1
 cap pnn_f64_short -k regex:pnn_f64_kernel_shared -o $O/pnn_f64_short python tools/prof.py --precision 64 --kind pnn --not-app 2mm,doitgen,gemm,pathfinder --restarts 32 --epochs 30 --reps 1
 cap lm_h1 -k regex:lm_warp_kernel -o $O/lm_h1 python tools/prof.py --kind br --app atax,bicg,syrk,covariance --restarts 32 --reps 1
+cap lm_warp32 -k regex:lm_warp_kernel -o $O/lm_warp32 python tools/prof.py --precision 64 --kind br --app gramschmit --restarts 32 --reps 1
