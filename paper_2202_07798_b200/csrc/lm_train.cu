@@ -568,6 +568,7 @@ __device__ void w_stats(WarpLm<PM>& S, const double* X, const double* Y, int n, 
 }
 
 // LU with partial pivoting (first maximal |pivot|, as idamax) + substitutions
+// (PM = 8: P <= 8)
 template <int PM>
 __device__ bool w_solve(WarpLm<PM>& S, int P, double alpha, double beta, double mu, int lane) {
   constexpr int LD = WarpLm<PM>::LD;
@@ -614,20 +615,42 @@ __device__ bool w_solve(WarpLm<PM>& S, int P, double alpha, double beta, double 
     }
     __syncwarp();
   }
-  for (int i = 0; i < P; ++i) {
-    double s = 0.0;
-    for (int j = lane; j < i; j += 32) s = fma(S.A[i * LD + j], S.rhs[j], s);
-    s = warp_sum(s);
-    if (lane == 0) S.rhs[i] = __dsub_rn(S.rhs[i], s);
-    __syncwarp();
+  // substitutions (P <= 8) by lane 0 in registers: the same row dot
+  // products and the same pairwise order as the warp reduction they replace
+  // (warp_sum over one term per lane: ((t0+t4)+(t2+t6)) + ((t1+t5)+(t3+t7))),
+  // so the results are unchanged, without the five dependent shuffles per row
+  if (lane == 0) {
+    auto tree8 = [](const double (&t)[8]) {
+      return ((t[0] + t[4]) + (t[2] + t[6])) + ((t[1] + t[5]) + (t[3] + t[7]));
+    };
+    double b[PM];
+#pragma unroll
+    for (int i = 0; i < PM; ++i) b[i] = i < P ? S.rhs[i] : 0.0;
+#pragma unroll
+    for (int i = 0; i < PM; ++i) {  // L y = b (unit diagonal), row i
+      if (i < P) {
+        double t[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) t[j] = j < i ? fma(S.A[i * LD + j], b[j], 0.0) : 0.0;
+        b[i] = __dsub_rn(b[i], tree8(t));
+        S.rhs[i] = b[i];
+      }
+    }
+#pragma unroll
+    for (int i = PM - 1; i >= 0; --i) {  // U x = y, row i (term L = column i+1+L)
+      if (i < P) {
+        double t[8];
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+          const int j = i + 1 + l;
+          t[l] = (j < PM && j < P) ? fma(S.A[i * LD + (j < PM ? j : 0)], b[j < PM ? j : 0], 0.0) : 0.0;
+        }
+        b[i] = div_safe_bf(__dsub_rn(b[i], tree8(t)), S.A[i * LD + i]);
+        S.delta[i] = b[i];
+      }
+    }
   }
-  for (int i = P - 1; i >= 0; --i) {
-    double s = 0.0;
-    for (int j = i + 1 + lane; j < P; j += 32) s = fma(S.A[i * LD + j], S.delta[j], s);
-    s = warp_sum(s);
-    if (lane == 0) S.delta[i] = div_safe_bf(__dsub_rn(S.rhs[i], s), S.A[i * LD + i]);
-    __syncwarp();
-  }
+  __syncwarp();
   return true;
 }
 
@@ -1141,8 +1164,8 @@ __device__ __forceinline__ void lm_fit_task(const LmLaunch& L, int64_t task, uns
         }
         if (!done) {
           tri = false;  // the LU overwrites the reflectors
-          solved = PM > 8 ? w_solve_cols<PM>(S, P, alpha, beta, mu, lane)
-                          : w_solve<PM>(S, P, alpha, beta, mu, lane);
+          if constexpr (PM > 8) solved = w_solve_cols<PM>(S, P, alpha, beta, mu, lane);
+          else solved = w_solve<PM>(S, P, alpha, beta, mu, lane);  // P <= 8 only
         }
         if (lane < P) S.wt[lane] = __dadd_rn(S.w[lane], S.delta[lane]);
       }
