@@ -582,18 +582,21 @@ __device__ bool w_solve(WarpLm<PM>& S, int P, double alpha, double beta, double 
   }
   __syncwarp();
   for (int k = 0; k < P; ++k) {
-    double best = (lane >= k && lane < P) ? fabs(S.A[lane * LD + k]) : -1.0;
-    int bi = lane;
+    // pivot: the first maximal |a_ik|, i >= k (idamax), scanned by lane 0
+    // (P <= 8 entries) and broadcast once
+    int bi = k;
+    if (lane == 0) {
+      double best = fabs(S.A[k * LD + k]);
 #pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, m);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, m);
-      if (ob > best || (ob == best && oi < bi)) {
-        best = ob;
-        bi = oi;
+      for (int i = 1; i < PM; ++i) {
+        const double v = (i > k && i < P) ? fabs(S.A[i * LD + k]) : -1.0;
+        if (v > best) {
+          best = v;
+          bi = i;
+        }
       }
     }
-    const int p = bi;
+    const int p = __shfl_sync(0xffffffffu, bi, 0);
     if (S.A[p * LD + k] == 0.0) return false;
     if (p != k) {
       if (lane < P) {
